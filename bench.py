@@ -1,0 +1,271 @@
+"""Benchmark: ADMM iterations/s on dense Lasso (BASELINE.json metric).
+
+Workload (BASELINE.json configs[4], the paper's billion-coefficient scale):
+dense Lasso 200000 x 5000 (1e9 coefficients), A ~ N(0,1) rounded to fp32,
+f = Square(b), g = lambda*Abs, built by the reference's Lasso recipe
+(instances.tall_lasso, bit-identical streams) on the host -- synthetic data.
+A is 4 GB in fp32, far larger than the 126 MB L2, so every timed iteration
+streams it from HBM (no L2 flush needed).
+
+A "step" is one ADMM iteration (solver.py:329-428) of that solve.
+  value  iterations/s with A resident in HBM: W warm-up iterations, then K
+         iterations timed with CUDA events on the solver's stream (barrier +
+         synchronize on both sides, max over ranks).
+  e2e    the same metric through the public API from HOST buffers: a full
+         ``solve(problem)`` on a pinned host copy of A -- H2D of A and the term
+         arrays, equilibration, Gram + Cholesky, iterations to eps_rel = 1e-3
+         and the D2H of x, y, mu, nu -- iterations / wall time.  Its wall time
+         is also reported as time_to_eps_s.
+  roofline  for the dominant kernel (row pass over A_hat), algorithmic bytes
+         m*n*4 per launch / its CUDA-event duration, against the measured HBM
+         copy peak (MEASURED_PEAKS.json).
+  cpu_baseline  the CPU oracle port (oracle/graphform_oracle.py, fp64 numpy
+         with all host threads) timed on a bounded row sample of the same
+         instance; iterations/s scaled to the full row count.
+
+--impl reference runs the CPU oracle port (the reference is pure Python and
+cannot travel to the GPU box) on the same full-size instance: prepare, then
+W + K iterations, timing the K.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M_FULL, N_FULL = 200_000, 5_000
+METRIC = "admm_iters_per_s"
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def build_instance(m, n, rank=0, world=1):
+    from paper_1503_08366_b200 import instances
+    prob, meta = instances.tall_lasso(m, n, seed=0, dtype=np.float32)
+    return prob, meta
+
+
+def cpu_baseline(prob, sample_rows, iters=10):
+    """Oracle port on the first `sample_rows` rows: iterations/s scaled to m."""
+    from oracle import graphform_oracle as orc
+    m = prob.m
+    A = np.asarray(prob.A[:sample_rows], dtype=np.float64)
+    f = orc.Terms(*(np.asarray(getattr(prob.f, k))[:sample_rows] for k in "habcde"))
+    g = orc.Terms.of(prob.g)
+    st = dict(abs_tol=1e-12, rel_tol=1e-12, max_iter=iters + 2)
+    setup = orc.prepare(A, st)
+    stamps = []
+    orc.solve(A, f, g, st, setup=setup, callback=lambda *a: stamps.append(time.perf_counter()))
+    dt = stamps[-1] - stamps[1]
+    per_it = dt / (len(stamps) - 2)
+    return {"value": (1.0 / per_it) * (sample_rows / m), "unit": "iters/s", "cores": os.cpu_count(),
+            "kind": "port",
+            "sample": f"first {sample_rows} of {m} rows ({sample_rows}x{prob.n} fp64), "
+                      f"{len(stamps) - 2} timed iterations after prepare; iters/s scaled by {sample_rows}/{m}"}
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    from oracle import graphform_oracle as orc
+    m, n = args.m, args.n
+    prob, _ = build_instance(m, n)
+    A = np.asarray(prob.A, dtype=np.float64)
+    f, g = orc.Terms.of(prob.f), orc.Terms.of(prob.g)
+    st = dict(abs_tol=1e-12, rel_tol=1e-12, max_iter=args.warmup + args.steps)
+    t0 = time.perf_counter()
+    setup = orc.prepare(A, st)
+    t_setup = time.perf_counter() - t0
+    stamps = []
+    orc.solve(A, f, g, st, setup=setup, callback=lambda *a: stamps.append(time.perf_counter()))
+    k = args.steps
+    dt = stamps[args.warmup + k - 1] - stamps[args.warmup - 1]
+    val = k / dt
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "iters/s", "n_gpus": world,
+            "steps": k, "warmup": args.warmup, "ms_per_step": 1e3 * dt / k, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"dense Lasso {m}x{n} (tall_lasso seed 0, A rounded to fp32, fp64 arithmetic)",
+                       "m": m, "n": n, "parallelism": "cpu"},
+            "cpu_baseline": {"value": val, "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"full instance; prepare {t_setup:.1f}s excluded; {k} iterations "
+                                       f"after {args.warmup} warm-up"},
+            "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import paper_1503_08366_b200 as gf
+    from paper_1503_08366_b200 import _native, solver as slv
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        raise SystemExit("multi-GPU bench is not wired in this build yet")
+    m, n = args.m, args.n
+    prob, meta = build_instance(m, n)
+    dev = torch.device("cuda", local)
+    peaks, peaks_kind = measured_peaks()
+    # ---------------- e2e: full solve from pinned host memory ----------------
+    A_pin = torch.from_numpy(prob.A).pin_memory()
+    prob_pin = gf.GraphFormProblem(A_pin, prob.f, prob.g)
+    e2e_runs = []
+    for _ in range(2):   # first call warms module load / allocator
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = gf.solve(prob_pin)
+        torch.cuda.synchronize()
+        e2e_runs.append((time.perf_counter() - t0, res))
+    e2e_time, res = e2e_runs[-1]
+    h2d = prob.A.nbytes + sum(getattr(prob.f, k).nbytes for k in "abcde") + m \
+        + sum(getattr(prob.g, k).nbytes for k in "abcde") + n
+    d2h = 8 * (2 * m + 2 * n)
+    # ---------------- device-resident iteration timing ----------------
+    setup = gf.prepare(prob)
+    tight = gf.SolverSettings(abs_tol=1e-12, rel_tol=1e-12, max_iter=args.warmup + 2 * args.steps + 8)
+    run = slv._Run(setup, prob.f, prob.g, tight, None, None, m)
+    run.run(args.warmup)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    L = _native.lib()
+    import ctypes as C
+    l0 = C.c_int64()
+    _native.check(L.gf_solver_stats(run.handle, C.byref(l0), None, None))
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        st = run.run(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    l1 = C.c_int64()
+    _native.check(L.gf_solver_stats(run.handle, C.byref(l1), None, None))
+    assert st.status == 0 and st.k + 1 == args.warmup + args.steps, (st.status, st.k)
+    value = args.steps / (ms / 1e3)
+    # ---------------- per-kernel durations (profiled pass) ----------------
+    _native.check(L.gf_solver_profile(run.handle, 1))
+    run.run(args.steps)
+    kms = (C.c_double * 8)()
+    kcnt = (C.c_int64 * 8)()
+    _native.check(L.gf_solver_stats(run.handle, None, kms, kcnt))
+    names = ["ginv_gemv_xside", "row_pass_yside", "col_pass", "slab_reduce", "y_scalars", "controller",
+             "allreduce", "-"]
+    kernels = {names[i]: {"avg_ms": kms[i] / kcnt[i], "count": int(kcnt[i])} for i in range(8) if kcnt[i]}
+    es = 4 if setup.dtype == _native.GF_F32 else 8
+    alg_bytes = m * n * es
+    t_row = kernels["row_pass_yside"]["avg_ms"] / 1e3
+    achieved = alg_bytes / t_row / 1e9
+    peak = peaks["hbm_gbs"]
+    line = {
+        "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if es == 4 else "f64",
+        "data": "synthetic (reference Lasso recipe, seed 0, A rounded to fp32)",
+        "config": {"workload": f"dense Lasso {m}x{n} fp32 (BASELINE configs[4], 1e9 coefficients)",
+                   "m": m, "n": n, "parallelism": f"row partition x{world}",
+                   "l2": "A is 4 GB >> 126 MB L2; no flush needed"},
+        "e2e": {"value": res.iterations / e2e_time, "unit": "iters/s",
+                "h2d_bytes_per_step": int(h2d / max(res.iterations, 1)),
+                "d2h_bytes_per_step": int(d2h / max(res.iterations, 1)),
+                "time_to_eps_s": e2e_time, "iterations": res.iterations, "status": res.status.value,
+                "objective": res.objective, "setup_s": res.setup_time, "h2d_bytes_total": int(h2d)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "row_pass_yside",
+                     "algorithmic_bytes_per_launch": alg_bytes, "peak_kind": peaks_kind},
+        "kernels": kernels,
+        "gpu_launches": int(l1.value - l0.value),
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(prob, max(1, m // 10), iters=10)
+    if rank == 0:
+        print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--m", type=int, default=M_FULL)
+    ap.add_argument("--n", type=int, default=N_FULL)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,517 @@
+// C-ABI entry points (include/graphform_b200.h): argument checks, object
+// lifetimes, error-code mapping, projector/setup orchestration and NCCL glue.
+
+#include <chrono>
+#include <cstring>
+
+#include "gf_internal.h"
+#include "gf_gemv.cuh"
+
+// implemented in gf_solver.cu
+gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, const gf_settings* st_in,
+                         const double* x0, const double* nu0, cudaStream_t st);
+void solver_run(gf_solver* s, int64_t steps, gf_solver_state* out, cudaStream_t st);
+void solver_history(gf_solver* s, int64_t count, double* out, cudaStream_t st);
+void solver_snapshot(gf_solver* s, double* x_hat, double* y_hat, double* xt, double* yt, double* xhh, double* yhh,
+                     cudaStream_t st);
+void solver_result(gf_solver* s, double* x, double* y, double* mu, double* nu, gf_solver_state* out,
+                   cudaStream_t st);
+double solver_elapsed(gf_solver* s);
+void solver_stats(gf_solver* s, int64_t* launches, double* kernel_ms, int64_t* kernel_count);
+void solver_profile(gf_solver* s, int enable);
+void solver_free(gf_solver* s);
+
+namespace gf {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error() { return g_last_error.c_str(); }
+void throw_error(int code, const std::string& msg) { throw Error{code, msg}; }
+
+int num_sms() {
+  static thread_local int dev = -1, sms = 0;
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d != dev) {
+    GF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d));
+    dev = d;
+  }
+  return sms;
+}
+
+void allreduce_sum(gf_comm* c, double* buf, size_t count, cudaStream_t st) {
+  if (c == nullptr || c->nranks <= 1 || count == 0) return;
+  const ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, st);
+  if (r != ncclSuccess) throw_error(GF_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+}
+
+template <typename F>
+static int guarded(F&& fn) {
+  try {
+    fn();
+    return GF_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return GF_E_CUDA;
+  }
+}
+
+static bool host_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return !(at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged);
+}
+
+// fp64 vector argument that may live on the host: device view (copied if needed).
+struct DevVec {
+  const double* p = nullptr;
+  DBuf own;
+  DevVec(const double* src, int64_t n, cudaStream_t st) {
+    if (src == nullptr || n <= 0) { p = src; return; }
+    if (host_ptr(src)) {
+      own.alloc(n * sizeof(double));
+      copy_in(own.as<double>(), src, n, st);
+      p = own.as<double>();
+    } else {
+      p = src;
+    }
+  }
+};
+
+__global__ void combine_kernel(const double* a, double sa, const double* b, double sb, double* out, int64_t n) {
+  for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    out[j] = sa * a[j] + sb * b[j];
+}
+static void combine(const double* a, double sa, const double* b, double sb, double* out, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  combine_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 1024), 256, 0, st>>>(a, sa, b, sb, out, n);
+  GF_CHECK_LAUNCH();
+}
+
+static void check_terms(const gf_terms* t) {
+  GF_REQUIRE(t != nullptr, GF_E_PARAMETER, "terms must not be NULL");
+  GF_REQUIRE(t->n >= 0, GF_E_DIMENSION, "negative length");
+  GF_REQUIRE(t->n == 0 || (t->h && t->a && t->b && t->c && t->d && t->e), GF_E_PARAMETER, "null term array");
+}
+
+static gf_projector* projector_build(gf_matrix* A, int mode, double tol, int64_t max_inner, gf_comm* comm,
+                                     cudaStream_t st) {
+  GF_REQUIRE(mode == 0 || mode == 1, GF_E_PARAMETER, "unknown projection mode");
+  GF_REQUIRE(tol > 0.0, GF_E_PARAMETER, "projection tolerance must be positive");
+  std::unique_ptr<gf_projector> P(new gf_projector());
+  P->A = A;
+  P->mode = mode;
+  P->comm = comm;
+  P->tall = A->m >= A->n;   // projection.py:76 (global rows decide under a partition)
+  if (comm && comm->nranks > 1) {
+    DBuf b(sizeof(double));
+    double mloc = (double)A->m;
+    GF_CUDA(cudaMemcpyAsync(b.p, &mloc, sizeof(double), cudaMemcpyHostToDevice, st));
+    allreduce_sum(comm, b.as<double>(), 1, st);
+    double mg = 0;
+    GF_CUDA(cudaMemcpyAsync(&mg, b.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    GF_CUDA(cudaStreamSynchronize(st));
+    P->tall = mg >= (double)A->n;
+    GF_REQUIRE(P->tall, GF_E_UNSUPPORTED, "row-partitioned solves require a tall matrix");
+  }
+  P->q = P->tall ? A->n : A->m;
+  P->tol = tol;
+  P->max_inner = max_inner > 0 ? max_inner : std::max<int64_t>(100, 2 * std::min(A->m, A->n));
+  if (mode == 1) return P.release();
+  const int64_t q = P->q;
+  P->ldg = padded_ld(q, GF_F64);
+  P->ldq = padded_ld(q, A->dtype);
+  const size_t gbytes = (size_t)std::max<int64_t>(q, 1) * P->ldg * sizeof(double);
+  P->gram.alloc(gbytes);
+  GF_CUDA(cudaMemsetAsync(P->gram.p, 0, gbytes, st));
+  if (A->m > 0 && A->n > 0) gram_accumulate(A, P->tall, P->gram.as<double>(), P->ldg, st);
+  if (comm && comm->nranks > 1) allreduce_sum(comm, P->gram.as<double>(), (size_t)q * P->ldg, st);
+  gram_finish(P->gram.as<double>(), q, P->ldg, st);
+  DBuf L(gbytes), tmp(gbytes), inv(gbytes), info(sizeof(int));
+  GF_CUDA(cudaMemcpyAsync(L.p, P->gram.p, gbytes, cudaMemcpyDeviceToDevice, st));
+  const int bad = cholesky(L.as<double>(), q, P->ldg, info.as<int>(), st);
+  if (bad != 0)
+    throw_error(GF_E_NUMERIC, "Gram factorization failed: leading minor of order " + std::to_string(bad) +
+                                  " is not positive definite");
+  GF_CUDA(cudaMemsetAsync(tmp.p, 0, gbytes, st));
+  trtri(L.as<double>(), q, P->ldg, tmp.as<double>(), st);
+  inverse_from_factor_inv(L.as<double>(), q, P->ldg, inv.as<double>(), st);
+  P->ginv.alloc((size_t)std::max<int64_t>(q, 1) * P->ldq * A->esize());
+  store_matrix(inv.as<double>(), P->ldg, A->dtype, P->ginv.p, P->ldq, q, q, st);
+  GF_CUDA(cudaStreamSynchronize(st));
+  return P.release();
+}
+
+static void ginv_apply(gf_projector* P, const double* rhs, double* out, cudaStream_t st) {
+  gf_matrix G;
+  G.dtype = P->A->dtype;
+  G.m = P->q; G.n = P->q; G.ld = P->ldq; G.data = P->ginv.p;
+  matvec(&G, false, rhs, out, st);
+}
+
+static void project_direct(gf_projector* P, const double* c, const double* d, double* x, double* y, cudaStream_t st) {
+  gf_matrix* A = P->A;
+  const int64_t m = A->m, n = A->n;
+  if (P->tall) {
+    DBuf t(std::max<int64_t>(n, 1) * sizeof(double)), rhs(std::max<int64_t>(n, 1) * sizeof(double));
+    GF_CUDA(cudaMemsetAsync(t.p, 0, t.bytes, st));
+    if (m > 0) matvec(A, true, d, t.as<double>(), st);                 // A' d
+    if (P->comm && P->comm->nranks > 1) allreduce_sum(P->comm, t.as<double>(), n, st);
+    combine(c, 1.0, t.as<double>(), 1.0, rhs.as<double>(), n, st);     // c + A' d
+    ginv_apply(P, rhs.as<double>(), x, st);                            // x = G^-1 (c + A' d)
+    if (m > 0) matvec(A, false, x, y, st);                             // y = A x
+  } else {
+    DBuf t(std::max<int64_t>(m, 1) * sizeof(double)), w(std::max<int64_t>(m, 1) * sizeof(double));
+    DBuf u(std::max<int64_t>(n, 1) * sizeof(double));
+    matvec(A, false, c, t.as<double>(), st);                           // A c
+    combine(t.as<double>(), 1.0, d, -1.0, t.as<double>(), m, st);      // A c - d
+    ginv_apply(P, t.as<double>(), w.as<double>(), st);                 // w
+    combine(d, 1.0, w.as<double>(), 1.0, y, m, st);                    // y = d + w
+    matvec(A, true, w.as<double>(), u.as<double>(), st);
+    combine(c, 1.0, u.as<double>(), -1.0, x, n, st);                   // x = c - A' w
+  }
+  GF_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace gf
+
+using namespace gf;
+
+struct gf_solver;
+extern "C" {
+
+const char* gf_version(void) { return "graphform-b200 0.1.0 (sm_100a)"; }
+const char* gf_last_error(void) { return gf::last_error(); }
+
+int gf_init(int device) {
+  return guarded([&] {
+    GF_CUDA(cudaSetDevice(device));
+    GF_CUDA(cudaFree(0));
+    num_sms();
+  });
+}
+
+int gf_prox_separable(const gf_terms* t, const double* rho, const double* v, double* out, void* stream) {
+  return guarded([&] {
+    check_terms(t);
+    TermsView view{t->h, t->a, t->b, t->c, t->d, t->e};
+    prox_separable(view, t->n, rho, v, out, (cudaStream_t)stream);
+    GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  });
+}
+
+int gf_prox_base(int64_t n, int kind, const double* rho, const double* v, double* out, void* stream) {
+  return guarded([&] {
+    GF_REQUIRE(kind >= 0 && kind <= 9, GF_E_PARAMETER, "unknown base function code");
+    prox_base(kind, n, rho, v, out, (cudaStream_t)stream);
+    GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  });
+}
+
+int gf_evaluate(const gf_terms* t, const double* v, double* result, void* stream) {
+  return guarded([&] {
+    check_terms(t);
+    TermsView view{t->h, t->a, t->b, t->c, t->d, t->e};
+    *result = evaluate(view, t->n, v, (cudaStream_t)stream);
+  });
+}
+
+int gf_eval_base(int64_t n, int kind, const double* x, double* out, void* stream) {
+  return guarded([&] {
+    GF_REQUIRE(kind >= 0 && kind <= 9, GF_E_PARAMETER, "unknown base function code");
+    eval_base(kind, n, x, out, (cudaStream_t)stream);
+    GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  });
+}
+
+int gf_matrix_create(int dtype, int64_t m, int64_t n, const void* src, int src_dtype, int64_t src_ld, void* stream,
+                     gf_matrix** out) {
+  return guarded([&] {
+    GF_REQUIRE(dtype == GF_F32 || dtype == GF_F64, GF_E_PARAMETER, "dtype must be GF_F32 or GF_F64");
+    GF_REQUIRE(src_dtype == GF_F32 || src_dtype == GF_F64, GF_E_PARAMETER, "bad source dtype");
+    GF_REQUIRE(m >= 0 && n >= 1, GF_E_DIMENSION, "matrix must have at least one column");
+    GF_REQUIRE(src != nullptr || m == 0, GF_E_PARAMETER, "null matrix");
+    GF_REQUIRE(src_ld >= n, GF_E_DIMENSION, "leading dimension smaller than n");
+    std::unique_ptr<gf_matrix> M(new gf_matrix());
+    M->dtype = dtype;
+    M->m = m;
+    M->n = n;
+    M->ld = padded_ld(n, dtype);
+    const size_t bytes = (size_t)std::max<int64_t>(m, 1) * M->ld * M->esize();
+    GF_CUDA(cudaMalloc(&M->data, bytes));
+    if (m > 0) matrix_upload(M.get(), src, src_dtype, src_ld, (cudaStream_t)stream);
+    GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    *out = M.release();
+  });
+}
+
+int gf_matrix_destroy(gf_matrix* A) {
+  return guarded([&] {
+    if (A == nullptr) return;
+    if (A->data) cudaFree(A->data);
+    delete A;
+  });
+}
+
+int gf_matrix_shape(const gf_matrix* A, int64_t* m, int64_t* n, int64_t* ld, int* dtype) {
+  return guarded([&] {
+    if (m) *m = A->m;
+    if (n) *n = A->n;
+    if (ld) *ld = A->ld;
+    if (dtype) *dtype = A->dtype;
+  });
+}
+
+int gf_matrix_download(const gf_matrix* A, double* dst, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (A->m == 0) return;
+    DBuf tmp((size_t)A->m * A->n * sizeof(double));
+    matrix_to_f64(A, tmp.as<double>(), st);
+    GF_CUDA(cudaMemcpyAsync(dst, tmp.p, (size_t)A->m * A->n * 8, cudaMemcpyDefault, st));
+    GF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int gf_matvec(const gf_matrix* A, int transpose, const double* x, double* y, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nx = transpose ? A->m : A->n, ny = transpose ? A->n : A->m;
+    DevVec xv(x, nx, st);
+    const bool yhost = ny > 0 && host_ptr(y);
+    DBuf yb;
+    double* yd = y;
+    if (yhost) { yb.alloc(ny * sizeof(double)); yd = yb.as<double>(); }
+    if (ny > 0 && nx > 0) matvec(A, transpose != 0, xv.p, yd, st);
+    if (yhost) copy_out(y, yd, ny, st);
+    GF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int gf_equilibrate(gf_matrix* A, double gamma, double eps, int64_t max_iter, gf_comm* comm, double* d, double* e,
+                   int64_t* sweeps, int* converged, double* gamma_used, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    DBuf dd(std::max<int64_t>(A->m, 1) * sizeof(double)), ee(A->n * sizeof(double));
+    const EquilResult r = equilibrate(A, gamma, eps, max_iter, comm, dd.as<double>(), ee.as<double>(), st);
+    copy_out(d, dd.as<double>(), A->m, st);
+    copy_out(e, ee.as<double>(), A->n, st);
+    GF_CUDA(cudaStreamSynchronize(st));
+    if (sweeps) *sweeps = r.sweeps;
+    if (converged) *converged = r.converged ? 1 : 0;
+    if (gamma_used) *gamma_used = r.gamma;
+  });
+}
+
+int gf_rescale_even(gf_matrix* A, double* d, double* e, gf_comm* comm, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    DBuf dd(std::max<int64_t>(A->m, 1) * sizeof(double)), ee(A->n * sizeof(double));
+    copy_in(dd.as<double>(), d, A->m, st);
+    copy_in(ee.as<double>(), e, A->n, st);
+    rescale_even(A, dd.as<double>(), ee.as<double>(), comm, st);
+    copy_out(d, dd.as<double>(), A->m, st);
+    copy_out(e, ee.as<double>(), A->n, st);
+    GF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int gf_scale_matrix(gf_matrix* A, const double* d, const double* e, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    DevVec dv(d, A->m, st), ev(e, A->n, st);
+    scale_matrix(A, dv.p, ev.p, st);
+    GF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int gf_projector_create(gf_matrix* A, int mode, double tol, int64_t max_inner, gf_comm* comm, void* stream,
+                        gf_projector** out) {
+  return guarded([&] { *out = projector_build(A, mode, tol, max_inner, comm, (cudaStream_t)stream); });
+}
+
+int gf_projector_destroy(gf_projector* P) {
+  return guarded([&] { delete P; });
+}
+
+int gf_projector_gram(const gf_projector* P, double* out, void* stream) {
+  return guarded([&] {
+    GF_REQUIRE(P->mode == 0, GF_E_PARAMETER, "indirect projectors have no Gram matrix");
+    cudaStream_t st = (cudaStream_t)stream;
+    GF_CUDA(cudaMemcpy2DAsync(out, P->q * sizeof(double), P->gram.p, P->ldg * sizeof(double), P->q * sizeof(double),
+                              P->q, cudaMemcpyDefault, st));
+    GF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int gf_project(gf_projector* P, const double* c, const double* d, double* x, double* y, void* stream) {
+  return guarded([&] {
+    GF_REQUIRE(P->mode == 0, GF_E_PARAMETER, "project requires a direct-mode cache; use project_indirect");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t m = P->A->m, n = P->A->n;
+    DevVec cv(c, n, st), dv(d, m, st);
+    DBuf xb(std::max<int64_t>(n, 1) * sizeof(double)), yb(std::max<int64_t>(m, 1) * sizeof(double));
+    project_direct(P, cv.p, dv.p, xb.as<double>(), yb.as<double>(), st);
+    copy_out(x, xb.as<double>(), n, st);
+    copy_out(y, yb.as<double>(), m, st);
+    GF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int gf_project_indirect(gf_projector* P, const double* c, const double* d, const double* x_warm,
+                        const double* y_warm, double tol, double* x, double* y, int64_t* iterations, int* converged,
+                        void* stream) {
+  (void)P; (void)c; (void)d; (void)x_warm; (void)y_warm; (void)tol; (void)x; (void)y; (void)iterations;
+  (void)converged; (void)stream;
+  set_error("project_indirect (CGLS) is not available in this build");
+  return GF_E_UNSUPPORTED;
+}
+
+int gf_setup_create(gf_matrix* A, int equil, const double* d_in, const double* e_in, int mode, double tol,
+                    int64_t max_inner, gf_comm* comm, void* stream, gf_setup** out) {
+  return guarded([&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    const auto t0 = std::chrono::steady_clock::now();
+    std::unique_ptr<gf_setup> S(new gf_setup());
+    S->comm = comm;
+    S->d.alloc(std::max<int64_t>(A->m, 1) * sizeof(double));
+    S->e.alloc(A->n * sizeof(double));
+    S->info.sweeps = 0;
+    S->info.converged = 1;
+    S->info.gamma = 0.0;
+    if (d_in != nullptr && e_in != nullptr) {
+      copy_in(S->d.as<double>(), d_in, A->m, st);
+      copy_in(S->e.as<double>(), e_in, A->n, st);
+    } else if (equil) {
+      const EquilResult r = equilibrate(A, -1.0, -1.0, 300, comm, S->d.as<double>(), S->e.as<double>(), st);
+      rescale_even(A, S->d.as<double>(), S->e.as<double>(), comm, st);
+      S->info.sweeps = r.sweeps;
+      S->info.converged = r.converged ? 1 : 0;
+      S->info.gamma = r.gamma;
+    } else {
+      std::vector<double> ones(std::max(A->m, A->n), 1.0);
+      copy_in(S->d.as<double>(), ones.data(), A->m, st);
+      copy_in(S->e.as<double>(), ones.data(), A->n, st);
+    }
+    scale_matrix(A, S->d.as<double>(), S->e.as<double>(), st);
+    S->P = projector_build(A, mode, tol, max_inner, comm, st);
+    S->A = A;  // ownership transferred on success only
+    GF_CUDA(cudaStreamSynchronize(st));
+    S->info.setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = S.release();
+  });
+}
+
+int gf_setup_destroy(gf_setup* S) {
+  return guarded([&] {
+    if (!S) return;
+    delete S->P;
+    if (S->A) gf_matrix_destroy(S->A);
+    delete S;
+  });
+}
+
+int gf_setup_get_info(const gf_setup* S, gf_setup_info* info) {
+  return guarded([&] { *info = S->info; });
+}
+
+int gf_setup_scaling(const gf_setup* S, double* d, double* e, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (d) copy_out(d, S->d.as<double>(), S->A->m, st);
+    if (e) copy_out(e, S->e.as<double>(), S->A->n, st);
+    GF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int gf_setup_projector(gf_setup* S, gf_projector** P) {
+  return guarded([&] { *P = S->P; });
+}
+
+int gf_setup_matrix(gf_setup* S, gf_matrix** A) {
+  return guarded([&] { *A = S->A; });
+}
+
+int gf_solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, const gf_settings* settings,
+                     const double* x0, const double* nu0, void* stream, gf_solver** out) {
+  return guarded([&] {
+    check_terms(f);
+    check_terms(g);
+    GF_REQUIRE(settings->max_iter >= 1, GF_E_PARAMETER, "max_iter must be at least 1");
+    *out = solver_create(S, f, g, settings, x0, nu0, (cudaStream_t)stream);
+  });
+}
+
+int gf_solver_run(gf_solver* s, int64_t steps, gf_solver_state* st, void* stream) {
+  return guarded([&] { solver_run(s, steps, st, (cudaStream_t)stream); });
+}
+
+int gf_solver_history(gf_solver* s, int64_t count, double* out, void* stream) {
+  return guarded([&] { solver_history(s, count, out, (cudaStream_t)stream); });
+}
+
+int gf_solver_snapshot(gf_solver* s, double* x_hat, double* y_hat, double* xt, double* yt, double* x_half_hat,
+                       double* y_half_hat, void* stream) {
+  return guarded([&] { solver_snapshot(s, x_hat, y_hat, xt, yt, x_half_hat, y_half_hat, (cudaStream_t)stream); });
+}
+
+int gf_solver_result(gf_solver* s, double* x, double* y, double* mu, double* nu, gf_solver_state* st, void* stream) {
+  return guarded([&] { solver_result(s, x, y, mu, nu, st, (cudaStream_t)stream); });
+}
+
+int gf_solver_destroy(gf_solver* s) {
+  return guarded([&] { solver_free(s); });
+}
+
+int gf_solver_elapsed_ms(gf_solver* s, double* ms) {
+  return guarded([&] { *ms = solver_elapsed(s); });
+}
+
+int gf_solver_stats(gf_solver* s, int64_t* launches, double* kernel_ms, int64_t* kernel_count) {
+  return guarded([&] { solver_stats(s, launches, kernel_ms, kernel_count); });
+}
+
+int gf_solver_profile(gf_solver* s, int enable) {
+  return guarded([&] { solver_profile(s, enable); });
+}
+
+int gf_comm_unique_id(char* id128) {
+  return guarded([&] {
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) throw_error(GF_E_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(id128, id.internal, sizeof(id.internal));
+  });
+}
+
+int gf_comm_create(const char* id128, int nranks, int rank, gf_comm** out) {
+  return guarded([&] {
+    GF_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, GF_E_PARAMETER, "bad rank / world size");
+    std::unique_ptr<gf_comm> c(new gf_comm());
+    c->nranks = nranks;
+    c->rank = rank;
+    if (nranks > 1) {
+      ncclUniqueId id;
+      std::memcpy(id.internal, id128, sizeof(id.internal));
+      const ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+      if (r != ncclSuccess) throw_error(GF_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    *out = c.release();
+  });
+}
+
+int gf_comm_destroy(gf_comm* c) {
+  return guarded([&] {
+    if (!c) return;
+    if (c->comm) ncclCommDestroy(c->comm);
+    delete c;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,120 @@
+// Internal object layouts and cross-file declarations of the C-ABI library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "gf_common.cuh"
+#include "gf_terms.cuh"
+
+// ------------------------------------------------------------- objects --
+struct gf_matrix {
+  int dtype = GF_F64;     // arithmetic type of the stored matrix
+  int64_t m = 0, n = 0;   // logical shape (this rank's rows)
+  int64_t ld = 0;         // padded row stride (elements)
+  void* data = nullptr;   // device, m * ld elements
+  size_t esize() const { return dtype == GF_F32 ? 4 : 8; }
+};
+
+struct gf_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+};
+
+namespace gf {
+
+// Device buffer with RAII free.
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  explicit DBuf(size_t b) { alloc(b); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DBuf& operator=(DBuf&& o) noexcept { std::swap(p, o.p); std::swap(bytes, o.bytes); return *this; }
+  ~DBuf() { if (p) cudaFree(p); }
+  void alloc(size_t b) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = b;
+    if (b) GF_CUDA(cudaMalloc(&p, b));
+  }
+  template <typename T> T* as() const { return (T*)p; }
+};
+
+// ------------------------------------------------ dense setup (gf_dense) --
+void gram_accumulate(const gf_matrix* A, bool tall, double* G, int64_t ldg, cudaStream_t st);
+void gram_finish(double* G, int64_t q, int64_t ldg, cudaStream_t st);
+int cholesky(double* G, int64_t q, int64_t ld, int* d_info, cudaStream_t st);
+void trtri(double* L, int64_t q, int64_t ld, double* tmp, cudaStream_t st);
+void inverse_from_factor_inv(const double* W, int64_t q, int64_t ld, double* Ginv, cudaStream_t st);
+void store_matrix(const double* src, int64_t lds, int dtype, void* dst, int64_t ldd, int64_t rows,
+                  int64_t cols, cudaStream_t st);
+
+// --------------------------------------------------- matrices (gf_matrix) --
+void matrix_upload(gf_matrix* M, const void* src, int src_dtype, int64_t src_ld, cudaStream_t st);
+void matrix_to_f64(const gf_matrix* M, double* dst_dev, cudaStream_t st);  // dense m x n
+void scale_matrix(gf_matrix* M, const double* d, const double* e, cudaStream_t st);
+// y = A x (x: n) / y = A' x (x: m); fp64 device vectors; ws >= matvec_ws_bytes.
+void matvec(const gf_matrix* A, bool transpose, const double* x, double* y, cudaStream_t st);
+
+// ---------------------------------------------- equilibration (gf_equil) --
+struct EquilResult {
+  int64_t sweeps;
+  bool converged;
+  double gamma;
+};
+EquilResult equilibrate(gf_matrix* A, double gamma, double eps, int64_t max_iter, gf_comm* comm,
+                        double* d_dev, double* e_dev, cudaStream_t st);
+void rescale_even(gf_matrix* A, double* d_dev, double* e_dev, gf_comm* comm, cudaStream_t st);
+
+// --------------------------------------------------- vectors (gf_vec.cu) --
+// Device copy of a gf_terms (h int8 + five fp64 arrays), owned.
+struct TermsDev {
+  DBuf buf;
+  int64_t n = 0;
+  TermsView view{};
+  void load(const gf_terms* t, cudaStream_t st);
+};
+void prox_separable(const TermsView& t, int64_t n, const double* rho, const double* v, double* out,
+                    cudaStream_t st);
+void prox_base(int kind, int64_t n, const double* rho, const double* v, double* out, cudaStream_t st);
+double evaluate(const TermsView& t, int64_t n, const double* v, cudaStream_t st);
+void eval_base(int kind, int64_t n, const double* x, double* out, cudaStream_t st);
+
+// ------------------------------------------------------------- NCCL glue --
+void allreduce_sum(gf_comm* c, double* buf, size_t count, cudaStream_t st);
+
+// Pointer helpers: copy host-or-device fp64 arrays.
+void copy_in(double* dst_dev, const double* src, int64_t n, cudaStream_t st);
+void copy_out(double* dst, const double* src_dev, int64_t n, cudaStream_t st);
+
+}  // namespace gf
+
+struct gf_projector {
+  gf_matrix* A = nullptr;   // not owned
+  int mode = 0;             // 0 direct, 1 indirect
+  bool tall = true;
+  int64_t q = 0, ldq = 0;   // reduced dimension, padded stride of Ginv
+  double tol = 1e-8;
+  int64_t max_inner = 100;
+  gf::DBuf gram;            // fp64 q x ldg (I + A'A or I + AA')
+  int64_t ldg = 0;
+  gf::DBuf ginv;            // working dtype, q x ldq: (I + A'A)^-1
+  gf_comm* comm = nullptr;
+};
+
+struct gf_setup {
+  gf_matrix* A = nullptr;   // owned: A_hat = D A E after creation
+  gf::DBuf d, e;            // fp64 scalings (m local, n)
+  gf_projector* P = nullptr;
+  gf_setup_info info{};
+  gf_comm* comm = nullptr;
+};

@@ -1,0 +1,701 @@
+// ADMM graph-projection-splitting iteration (reference solver.py:248-437).
+//
+// Data layout in HBM (per rank, tall problems m >= n, row partition):
+//   A_hat    m x ld   working dtype T (fp32/fp64), scaled in place by setup
+//   Ginv     q x ldq  T, (I + A_hat' A_hat)^-1, q = n
+//   x side   n-vectors fp64: x^, x~, c_x, x_1/2 [2], mu^_1/2 [2]  (+ T copies of
+//            x^, x^_1/2 and rhs as the GEMV right-hand sides)
+//   y side   m-vectors fp64: y^, y~, c_y, y_1/2 [2], nu^_1/2 [2]
+// The half iterates are double-buffered by iteration parity so a degenerate
+// iteration can hand back the previous one (solver.py:337-342).
+//
+// One iteration k is four launches (the per-iteration schedule of SURVEY
+// §7.2, which reads A_hat twice and never touches the unscaled A):
+//   R(k)  row pass    A_hat [x^, x^_1/2] with the whole y side in the epilogue:
+//                     y~ update (dual step + adaptive-rho rescale of k-1),
+//                     prox_f, nu^_1/2, c_y, and the r_pri / ||y|| / f(y)
+//                     partials (r_pri = ||D^-1 (A_hat x^_1/2 - y^_1/2)||).
+//   C(k)  column pass A_hat' [c_y, nu^_1/2] -> per-slab partials
+//   Z(k)  slab reduce (+ NCCL all-reduce of [2n + 6] under a row partition),
+//         rhs = c_x + A_hat' c_y, r_dual = ||E^-1 (A_hat' nu^ + mu^)||, and in
+//         the last CTA the controller: stop rule (solver.py:191-202, 373-376),
+//         degenerate checks, history row, adaptive rho (solver.py:221-239).
+//   S(k)  x+ = Ginv rhs (GEMV) with the whole x side in the epilogue:
+//         x~ update, prox_g for iteration k+1, mu^_1/2, c_x, ||mu||, g(x).
+// The controller lives on the device, so a chunk of iterations runs without a
+// host round trip; kernels of iterations after termination return at entry.
+
+#include "gf_internal.h"
+#include "gf_gemv.cuh"
+
+namespace gf {
+
+struct Ctl {
+  int status;
+  unsigned ticket;
+  int64_t k;           // iteration being assembled (R/C/Z) / prepared (S)
+  int64_t iterations;  // SolveResult.iterations once terminated
+  int64_t last_good;   // last recorded iteration, -1 if none
+  int64_t l_mark, u_mark;
+  int64_t inner;       // CGLS inner iterations of the last projection
+  double rho, rho_prev, ratio, final_rho;
+  double r_pri, r_dual, eps_pri, eps_dual, objective;
+};
+
+struct Params {
+  double abs_tol, rel_tol, alpha, delta, tau;
+  int64_t max_iter;
+  int adaptive;
+};
+
+constexpr int kRedY = 4;  // r_pri^2, ||y||^2, f(y), drift_y^2 (+ flags)
+constexpr int kRedX = 3;  // ||mu||^2, g(x), drift_x^2 (+ flags)
+constexpr int kScal = 6;  // all-reduced scalars after the 2*ld column sums
+enum : unsigned { kBadXPlus = 1, kBadXHalf = 2, kBadYPlus = 4, kBadYHalf = 8 };
+
+template <typename T>
+struct YEpi {
+  static constexpr int NR = kRedY;
+  Ctl* ctl;
+  TermsView f;
+  const double* d;
+  double *yk, *yt, *cy, *yh2, *nuh2;
+  int64_t m;
+  double alpha;
+  int warm_x;
+  __device__ bool active() const { return ctl->status == GF_STATUS_RUNNING; }
+  __device__ void row(int64_t i, const double* dots, double* red, unsigned& flags) const {
+    const int64_t k = ctl->k;
+    const double rho = ctl->rho;
+    double ykv, ytv;
+    if (k == 0) {
+      ykv = warm_x ? dots[0] : yk[i];
+      ytv = yt[i];
+    } else {
+      ykv = dots[0];                          // y+ = A_hat x+  (projection.py:122)
+      ytv = (cy[i] - ykv) * ctl->ratio;       // y~ + r_y - y+, rescaled (solver.py:420, :237)
+    }
+    if (!isfinite(ykv)) flags |= kBadYPlus;
+    const double di = d[i];
+    const Term t = load_term(f, i);
+    const double yh = prox_term(t, rho * (di * di), (ykv - ytv) / di);  // solver.py:331-336
+    if (!isfinite(yh)) flags |= kBadYHalf;
+    const double yhh = yh * di;
+    const double nu = -rho * (yhh - ykv + ytv);                          // solver.py:180
+    const double ry = alpha * yhh + (1.0 - alpha) * ykv;                 // solver.py:394
+    const int64_t b = (k & 1) * m;
+    yk[i] = ykv;
+    yt[i] = ytv;
+    yh2[b + i] = yh;
+    nuh2[b + i] = nu;
+    cy[i] = ry + ytv;
+    const double rp = dots[1] / di - yh;    // (A x_1/2 - y_1/2)_i via A_hat
+    red[0] += rp * rp;
+    red[1] += yh * yh;
+    red[2] += eval_term(t, yh);
+    red[3] += (yhh - ykv) * (yhh - ykv);
+  }
+};
+
+template <typename T>
+struct XEpi {
+  static constexpr int NR = kRedX;
+  Ctl* ctl;
+  TermsView g;
+  const double* e;
+  double *xk, *xt, *cx, *xh2, *muh2;
+  T *xk_T, *xh_T;
+  int64_t n;
+  double alpha;
+  __device__ bool active() const { return ctl->status == GF_STATUS_RUNNING; }
+  // init: x^, x~ given (warm start or zero) -- iteration 0 has no dual step.
+  __device__ void apply(int64_t j, double xkv, double xtv, double* red, unsigned& flags) const {
+    const int64_t k1 = ctl->k;
+    const double rho = ctl->rho;
+    const double ej = e[j];
+    const Term t = load_term(g, j);
+    const double xh = prox_term(t, rho / (ej * ej), ej * (xkv - xtv));   // solver.py:330-335
+    if (!isfinite(xh)) flags |= kBadXHalf;
+    const double xhh = xh / ej;
+    const double mu = -rho * (xhh - xkv + xtv);                          // solver.py:179
+    const double rx = alpha * xhh + (1.0 - alpha) * xkv;                 // solver.py:393
+    const int64_t b = (k1 & 1) * n;
+    xk[j] = xkv;
+    xt[j] = xtv;
+    xh2[b + j] = xh;
+    muh2[b + j] = mu;
+    cx[j] = rx + xtv;
+    xk_T[j] = (T)xkv;
+    xh_T[j] = (T)xhh;
+    const double mo = mu / ej;
+    red[0] += mo * mo;
+    red[1] += eval_term(t, xh);
+    red[2] += (xhh - xkv) * (xhh - xkv);
+  }
+  __device__ void row(int64_t j, const double* dots, double* red, unsigned& flags) const {
+    const double xp = dots[0];                                           // x+ (projection.py:121)
+    if (!isfinite(xp)) flags |= kBadXPlus;
+    apply(j, xp, (cx[j] - xp) * ctl->ratio, red, flags);                 // solver.py:419, :237
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) x_init_kernel(XEpi<T> epi, double* __restrict__ part) {
+  double red[kRedX] = {0.0, 0.0, 0.0};
+  unsigned flags = 0;
+  for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < epi.n; j += (int64_t)gridDim.x * blockDim.x)
+    epi.apply(j, epi.xk[j], epi.xt[j], red, flags);
+  __shared__ double sh[8][kRedX + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kRedX; ++k) red[k] = warp_sum(red[k]);
+  flags = warp_or(flags);
+  if (lane == 0) {
+    for (int k = 0; k < kRedX; ++k) sh[warp][k] = red[k];
+    sh[warp][kRedX] = (double)flags;
+  }
+  __syncthreads();
+  if (threadIdx.x <= kRedX) {
+    const int k = threadIdx.x;
+    if (k < kRedX) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += sh[w][k];
+      part[blockIdx.x * (kRedX + 1) + k] = s;
+    } else {
+      unsigned f = 0;
+      for (int w = 0; w < 8; ++w) f |= (unsigned)sh[w][kRedX];
+      part[blockIdx.x * (kRedX + 1) + kRedX] = (double)f;
+    }
+  }
+}
+
+// Z1 scalars: reduce the R partials -> red[2*ld .. 2*ld+6):
+//   [r_pri^2, ||y||^2, f(y), drift_y^2, #bad y+, #bad y_1/2]
+__global__ void y_scalars_kernel(const double* __restrict__ rpart, int64_t count, double* __restrict__ out,
+                                 const Ctl* ctl) {
+  if (ctl->status != GF_STATUS_RUNNING) return;
+  __shared__ double sh[256];
+  __shared__ unsigned shf[256];
+  for (int k = 0; k < kRedY; ++k) {
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < count; i += blockDim.x) s += rpart[i * (kRedY + 1) + k];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+      if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[k] = sh[0];
+    __syncthreads();
+  }
+  unsigned f = 0;
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) f |= (unsigned)rpart[i * (kRedY + 1) + kRedY];
+  shf[threadIdx.x] = f;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int i = 0; i < 256; ++i) t |= shf[i];
+    out[4] = (t & kBadYPlus) ? 1.0 : 0.0;
+    out[5] = (t & kBadYHalf) ? 1.0 : 0.0;
+  }
+}
+
+// Z2: rhs and r_dual per column, then the controller in the last CTA.
+template <typename T>
+__global__ void __launch_bounds__(256)
+control_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ red, int64_t ld, int64_t n,
+               const double* __restrict__ cx, const double* __restrict__ e, const double* __restrict__ muh2,
+               T* __restrict__ rhs_T, double* __restrict__ zpart, const double* __restrict__ xpart,
+               int64_t nxpart, double* __restrict__ hist) {
+  if (ctl->status != GF_STATUS_RUNNING) return;
+  const int64_t k = ctl->k;
+  const double* muh = muh2 + (k & 1) * n;
+  double rd2 = 0.0;
+  for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double s1 = red[j], s2 = red[ld + j];
+    rhs_T[j] = (T)(cx[j] + s1);                       // c + A_hat' d (projection.py:121)
+    const double ej = e[j];
+    const double rdj = s2 / ej + muh[j] / ej;         // A' nu + mu in original space
+    rd2 += rdj * rdj;
+  }
+  __shared__ double sh[256];
+  __shared__ bool last;
+  sh[threadIdx.x] = rd2;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    zpart[blockIdx.x] = sh[0];
+    __threadfence();
+    const unsigned t = atomicAdd(&ctl->ticket, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // ---- last CTA: x-side partials of S(k-1) / x-init ----
+  double xs[kRedX + 1];
+  for (int q = 0; q < kRedX; ++q) {
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < nxpart; i += blockDim.x) s += xpart[i * (kRedX + 1) + q];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+      if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+      __syncthreads();
+    }
+    xs[q] = sh[0];
+    __syncthreads();
+  }
+  {
+    unsigned f = 0;
+    for (int64_t i = threadIdx.x; i < nxpart; i += blockDim.x) f |= (unsigned)xpart[i * (kRedX + 1) + kRedX];
+    sh[threadIdx.x] = (double)f;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned t = 0;
+      for (int i = 0; i < 256; ++i) t |= (unsigned)sh[i];
+      xs[kRedX] = (double)t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  double r2 = 0.0;
+  for (unsigned b = 0; b < gridDim.x; ++b) r2 += zpart[b];
+  ctl->ticket = 0;
+  const double* ys = red + 2 * ld;
+  const unsigned xf = (unsigned)xs[kRedX];
+  const bool proj_bad = (xf & kBadXPlus) || ys[4] > 0.0;
+  const bool prox_bad = (xf & kBadXHalf) || ys[5] > 0.0;
+  if (k >= prm.max_iter) {  // past the last iteration: only its projection check remains
+    ctl->iterations = prm.max_iter;
+    if (proj_bad) { ctl->status = GF_STATUS_DEGENERATE; ctl->final_rho = ctl->rho_prev; }
+    else { ctl->status = GF_STATUS_MAX_ITERATIONS; ctl->final_rho = ctl->rho; }
+    return;
+  }
+  if (proj_bad || prox_bad) {   // solver.py:337-341 / :414-417 -> previous half iterate
+    ctl->status = GF_STATUS_DEGENERATE;
+    ctl->iterations = k;
+    ctl->final_rho = proj_bad ? ctl->rho_prev : ctl->rho;
+    return;
+  }
+  const double rho = ctl->rho;
+  const double r_pri = sqrt(ys[0]);
+  const double r_dual = sqrt(r2);
+  const double eps_pri = prm.abs_tol + prm.rel_tol * sqrt(ys[1]);
+  const double eps_dual = prm.abs_tol + prm.rel_tol * sqrt(xs[0]);
+  const double obj = ys[2] + xs[1];
+  double* hrow = hist + k * 8;
+  hrow[0] = r_pri; hrow[1] = r_dual; hrow[2] = eps_pri; hrow[3] = eps_dual;
+  hrow[4] = rho; hrow[5] = obj; hrow[6] = sqrt(ys[3] + xs[2]); hrow[7] = (double)ctl->inner;
+  ctl->last_good = k;
+  ctl->r_pri = r_pri; ctl->r_dual = r_dual; ctl->eps_pri = eps_pri; ctl->eps_dual = eps_dual;
+  ctl->objective = obj;
+  if (r_pri <= eps_pri && r_dual <= eps_dual) {   // solver.py:201, :373-376
+    ctl->status = GF_STATUS_SOLVED;
+    ctl->iterations = k + 1;
+    ctl->final_rho = rho;
+    return;
+  }
+  double nrho = rho, ratio = 1.0;                  // adapt_rho, solver.py:221-239
+  if (prm.adaptive) {
+    if (r_dual < eps_dual && prm.tau * (double)k > (double)ctl->l_mark) {
+      nrho = prm.delta * rho;
+      ratio = rho / nrho;
+      ctl->u_mark = k;
+    } else if (r_pri < eps_pri && prm.tau * (double)k > (double)ctl->u_mark) {
+      nrho = rho / prm.delta;
+      ratio = rho / nrho;
+      ctl->l_mark = k;
+    }
+  }
+  ctl->rho_prev = rho;
+  ctl->rho = nrho;
+  ctl->ratio = ratio;
+  ctl->k = k + 1;
+}
+
+// ------------------------------------------------------------- results --
+__global__ void result_kernel(const Ctl* ctl, int64_t n, int64_t m, const double* __restrict__ xh2,
+                              const double* __restrict__ muh2, const double* __restrict__ yh2,
+                              const double* __restrict__ nuh2, const double* __restrict__ e,
+                              const double* __restrict__ d, double* x, double* mu, double* y, double* nu) {
+  const int64_t L = ctl->last_good;
+  const int64_t bx = (L & 1) * n, by = (L & 1) * m;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < n; j += stride) {
+    x[j] = L < 0 ? 0.0 : xh2[bx + j];
+    mu[j] = L < 0 ? 0.0 : muh2[bx + j] / e[j];       // unscale (solver.py:188)
+  }
+  for (int64_t i = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; i < m; i += stride) {
+    y[i] = L < 0 ? 0.0 : yh2[by + i];
+    nu[i] = L < 0 ? 0.0 : d[i] * nuh2[by + i];
+  }
+}
+
+__global__ void snapshot_kernel(const Ctl* ctl, int64_t n, int64_t m, const double* xh2, const double* yh2,
+                                const double* e, const double* d, double* xhh, double* yhh) {
+  const int64_t L = ctl->last_good < 0 ? 0 : ctl->last_good;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < n; j += stride) xhh[j] = xh2[(L & 1) * n + j] / e[j];
+  for (int64_t i = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; i < m; i += stride) yhh[i] = yh2[(L & 1) * m + i] * d[i];
+}
+
+__global__ void warm_init_kernel(const double* __restrict__ x0, const double* __restrict__ nu0, const double* e,
+                                 const double* d, int64_t n, int64_t m, double rho, double* xk, double* nuhat0,
+                                 double* yt) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < n; j += stride)
+    xk[j] = x0 ? x0[j] / e[j] : 0.0;                 // solver.py:301
+  for (int64_t i = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; i < m; i += stride) {
+    if (nu0) {
+      const double nh = nu0[i] / d[i];               // solver.py:304-305
+      nuhat0[i] = nh;
+      yt[i] = -nh / rho;
+    } else {
+      yt[i] = 0.0;
+    }
+  }
+}
+
+__global__ void div_into(const double* __restrict__ src, int64_t n, double rho, double* __restrict__ dst) {
+  for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    dst[j] = src[j] / rho;                           // solver.py:306
+}
+
+}  // namespace gf
+
+// ============================================================== driver ====
+using namespace gf;
+
+struct gf_solver {
+  gf_setup* S = nullptr;
+  int dtype = GF_F64;
+  int64_t m = 0, n = 0, ld = 0, q = 0, ldq = 0;
+  Params prm{};
+  TermsDev f, g;
+  DBuf ctl, hist;
+  DBuf xk, xt, cx, xh2, muh2, yk, yt, cy, yh2, nuh2;
+  DBuf xk_T, xh_T, rhs_T;
+  DBuf rpart, cpart, red, zpart, xpart;
+  int64_t grid_r = 1, grid_s = 1, grid_z = 1;
+  ColPlan cplan;
+  int warm_x = 0;
+  int64_t next_step = 0;  // step k = [S(k-1)], R(k), C(k), Z(k)
+  Ctl host{};
+  Ctl* pinned = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  double elapsed_ms = 0.0;
+  int64_t launches = 0;  // kernels launched by solver_run
+  // optional per-kernel timing (gf_solver_profile): events around each launch
+  bool profile = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> ev_marks;  // (kernel class, pool index of start event)
+  double kms[8] = {0};
+  int64_t kcount[8] = {0};
+  ~gf_solver() {
+    if (pinned) cudaFreeHost(pinned);
+    if (ev_a) cudaEventDestroy(ev_a);
+    if (ev_b) cudaEventDestroy(ev_b);
+    for (auto e : ev_pool) cudaEventDestroy(e);
+  }
+  // Kernel classes: 0 S (Ginv GEMV + x side), 1 R (row pass + y side),
+  // 2 C (column pass), 3 column-slab reduce, 4 y scalars, 5 controller,
+  // 6 NCCL all-reduce.
+  void mark(int cls, cudaStream_t st, bool begin) {
+    if (!profile) return;
+    const size_t idx = ev_marks.size() * 2 + (begin ? 0 : 1);
+    while (ev_pool.size() <= idx) {
+      cudaEvent_t e;
+      GF_CUDA(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    GF_CUDA(cudaEventRecord(ev_pool[idx], st));
+    if (!begin) ev_marks.emplace_back(cls, (int)(idx - 1));
+  }
+  void collect() {
+    for (auto& mk : ev_marks) {
+      float ms = 0.f;
+      GF_CUDA(cudaEventElapsedTime(&ms, ev_pool[mk.second], ev_pool[mk.second + 1]));
+      kms[mk.first] += ms;
+      kcount[mk.first] += 1;
+    }
+    ev_marks.clear();
+  }
+};
+
+namespace gf {
+
+template <typename T>
+static YEpi<T> make_yepi(gf_solver* s) {
+  YEpi<T> y;
+  y.ctl = s->ctl.as<Ctl>();
+  y.f = s->f.view;
+  y.d = s->S->d.as<double>();
+  y.yk = s->yk.as<double>(); y.yt = s->yt.as<double>(); y.cy = s->cy.as<double>();
+  y.yh2 = s->yh2.as<double>(); y.nuh2 = s->nuh2.as<double>();
+  y.m = s->m; y.alpha = s->prm.alpha; y.warm_x = s->warm_x;
+  return y;
+}
+
+template <typename T>
+static XEpi<T> make_xepi(gf_solver* s) {
+  XEpi<T> x;
+  x.ctl = s->ctl.as<Ctl>();
+  x.g = s->g.view;
+  x.e = s->S->e.as<double>();
+  x.xk = s->xk.as<double>(); x.xt = s->xt.as<double>(); x.cx = s->cx.as<double>();
+  x.xh2 = s->xh2.as<double>(); x.muh2 = s->muh2.as<double>();
+  x.xk_T = s->xk_T.as<T>(); x.xh_T = s->xh_T.as<T>();
+  x.n = s->n; x.alpha = s->prm.alpha;
+  return x;
+}
+
+template <typename T>
+static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
+  gf_matrix* A = s->S->A;
+  gf_projector* P = s->S->P;
+  Ctl* ctl = s->ctl.as<Ctl>();
+  if (k > 0) {  // S(k-1): x+ = Ginv rhs and the x side of iteration k
+    s->mark(0, st, true);
+    rowgemv_kernel<T, 1, XEpi<T>><<<(unsigned)s->grid_s, kRowThreads, 0, st>>>(
+        P->ginv.as<T>(), s->q, s->ldq, s->rhs_T.as<T>(), s->rhs_T.as<T>(), make_xepi<T>(s), s->xpart.as<double>());
+    GF_CHECK_LAUNCH();
+    s->mark(0, st, false);
+    s->launches += 1;
+  }
+  if (s->m > 0) {
+    s->mark(1, st, true);
+    rowgemv_kernel<T, 2, YEpi<T>><<<(unsigned)s->grid_r, kRowThreads, 0, st>>>(
+        (const T*)A->data, s->m, s->ld, s->xk_T.as<T>(), s->xh_T.as<T>(), make_yepi<T>(s), s->rpart.as<double>());
+    GF_CHECK_LAUNCH();
+    s->mark(1, st, false);
+    s->mark(2, st, true);
+    colgemv_kernel<T, 2, false><<<dim3((unsigned)s->cplan.col_blocks, (unsigned)s->cplan.slabs), kColThreads, 0, st>>>(
+        (const T*)A->data, s->m, s->ld, s->cy.as<double>(), s->nuh2.as<double>() + (k & 1) * s->m,
+        s->cplan.rows_per_slab, s->cpart.as<double>(), &ctl->status);
+    GF_CHECK_LAUNCH();
+    s->mark(2, st, false);
+    s->mark(3, st, true);
+    colreduce_kernel<<<dim3((unsigned)ceil_div(s->ld, 32), 2), dim3(32, 8), 0, st>>>(
+        s->cpart.as<double>(), s->cplan.slabs, s->ld, 2, s->red.as<double>(), &ctl->status);
+    GF_CHECK_LAUNCH();
+    s->mark(3, st, false);
+    s->mark(4, st, true);
+    y_scalars_kernel<<<1, 256, 0, st>>>(s->rpart.as<double>(), s->grid_r, s->red.as<double>() + 2 * s->ld, ctl);
+    GF_CHECK_LAUNCH();
+    s->mark(4, st, false);
+    s->launches += 4;
+  } else {
+    GF_CUDA(cudaMemsetAsync(s->red.p, 0, (2 * s->ld + kScal) * sizeof(double), st));
+  }
+  if (s->S->comm && s->S->comm->nranks > 1) {
+    s->mark(6, st, true);
+    allreduce_sum(s->S->comm, s->red.as<double>(), 2 * s->ld + kScal, st);
+    s->mark(6, st, false);
+  }
+  s->mark(5, st, true);
+  control_kernel<T><<<(unsigned)s->grid_z, 256, 0, st>>>(
+      ctl, s->prm, s->red.as<double>(), s->ld, s->n, s->cx.as<double>(), s->S->e.as<double>(), s->muh2.as<double>(),
+      s->rhs_T.as<T>(), s->zpart.as<double>(), s->xpart.as<double>(), s->grid_s, s->hist.as<double>());
+  GF_CHECK_LAUNCH();
+  s->mark(5, st, false);
+  s->launches += 1;
+}
+
+template <typename T>
+static void solver_init(gf_solver* s, const double* x0, const double* nu0, double rho0, cudaStream_t st) {
+  const int64_t n = s->n, m = s->m;
+  DBuf x0d, nu0d, nuhat0;
+  if (x0) { x0d.alloc(n * sizeof(double)); copy_in(x0d.as<double>(), x0, n, st); }
+  if (nu0) { nu0d.alloc(std::max<int64_t>(m, 1) * sizeof(double)); copy_in(nu0d.as<double>(), nu0, m, st); }
+  nuhat0.alloc(std::max<int64_t>(m, 1) * sizeof(double));
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max(n, m), 256), 2048));
+  warm_init_kernel<<<g, 256, 0, st>>>(x0 ? x0d.as<double>() : nullptr, nu0 ? nu0d.as<double>() : nullptr,
+                                      s->S->e.as<double>(), s->S->d.as<double>(), n, m, rho0, s->xk.as<double>(),
+                                      nuhat0.as<double>(), s->yt.as<double>());
+  GF_CHECK_LAUNCH();
+  GF_CUDA(cudaMemsetAsync(s->xt.p, 0, n * sizeof(double), st));
+  GF_CUDA(cudaMemsetAsync(s->yk.p, 0, std::max<int64_t>(m, 1) * sizeof(double), st));
+  if (nu0) {  // x~ = A_hat' nu^0 / rho (all-reduced under a row partition)
+    DBuf tmp(s->ld * sizeof(double));
+    GF_CUDA(cudaMemsetAsync(tmp.p, 0, s->ld * sizeof(double), st));
+    if (m > 0) matvec(s->S->A, true, nuhat0.as<double>(), tmp.as<double>(), st);
+    if (s->S->comm && s->S->comm->nranks > 1) allreduce_sum(s->S->comm, tmp.as<double>(), n, st);
+    div_into<<<g, 256, 0, st>>>(tmp.as<double>(), n, rho0, s->xt.as<double>());
+    GF_CHECK_LAUNCH();
+  }
+  x_init_kernel<T><<<(unsigned)s->grid_s, 256, 0, st>>>(make_xepi<T>(s), s->xpart.as<double>());
+  GF_CHECK_LAUNCH();
+  GF_CUDA(cudaStreamSynchronize(st));
+}
+
+static void read_ctl(gf_solver* s, cudaStream_t st) {
+  GF_CUDA(cudaMemcpyAsync(s->pinned, s->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+  GF_CUDA(cudaStreamSynchronize(st));
+  s->host = *s->pinned;
+}
+
+static void fill_state(gf_solver* s, gf_solver_state* st) {
+  const Ctl& c = s->host;
+  st->status = c.status;
+  st->iterations = c.status == GF_STATUS_RUNNING ? c.last_good + 1 : c.iterations;
+  st->k = c.last_good;
+  const bool rec = c.last_good >= 0;
+  st->r_pri = rec ? c.r_pri : INFINITY;
+  st->r_dual = rec ? c.r_dual : INFINITY;
+  st->eps_pri = rec ? c.eps_pri : NAN;
+  st->eps_dual = rec ? c.eps_dual : NAN;
+  st->objective = c.objective;
+  st->rho = c.rho;
+  st->final_rho = c.status == GF_STATUS_RUNNING ? c.rho : c.final_rho;
+  st->inner_iterations = c.inner;
+}
+
+}  // namespace gf
+
+// ---------------------------------------------------------- C++ entry points
+gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, const gf_settings* st_in,
+                         const double* x0, const double* nu0, cudaStream_t st) {
+  GF_REQUIRE(S->P != nullptr, GF_E_PARAMETER, "setup has no projector");
+  GF_REQUIRE(S->P->mode == 0, GF_E_UNSUPPORTED, "indirect projection is not available in this build");
+  GF_REQUIRE(S->P->tall, GF_E_UNSUPPORTED, "wide (m < n) problems are not available in this build");
+  std::unique_ptr<gf_solver> s(new gf_solver());
+  s->S = S;
+  gf_matrix* A = S->A;
+  s->dtype = A->dtype;
+  s->m = A->m; s->n = A->n; s->ld = A->ld; s->q = S->P->q; s->ldq = S->P->ldq;
+  GF_REQUIRE(f->n == s->m, GF_E_DIMENSION, "f length does not match the rows of A");
+  GF_REQUIRE(g->n == s->n, GF_E_DIMENSION, "g length does not match the columns of A");
+  s->prm = Params{st_in->abs_tol, st_in->rel_tol, st_in->alpha, st_in->delta, st_in->tau, st_in->max_iter,
+                  st_in->adaptive_rho};
+  s->f.load(f, st);
+  s->g.load(g, st);
+  const int sms = num_sms();
+  const int64_t n = s->n, m1 = std::max<int64_t>(s->m, 1), es = A->esize();
+  s->grid_r = row_grid(m1, sms);
+  s->grid_s = row_grid(s->q, sms);
+  s->grid_z = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 2 * (int64_t)sms));
+  s->cplan = plan_cols(m1, s->ld, s->dtype == GF_F32 ? 4 : 2, sms);
+  auto vec = [&](DBuf& b, int64_t len) { b.alloc(len * sizeof(double)); GF_CUDA(cudaMemsetAsync(b.p, 0, b.bytes, st)); };
+  vec(s->xk, n); vec(s->xt, n); vec(s->cx, n); vec(s->xh2, 2 * n); vec(s->muh2, 2 * n);
+  vec(s->yk, m1); vec(s->yt, m1); vec(s->cy, m1); vec(s->yh2, 2 * m1); vec(s->nuh2, 2 * m1);
+  auto tv = [&](DBuf& b, int64_t len) { b.alloc(len * es); GF_CUDA(cudaMemsetAsync(b.p, 0, b.bytes, st)); };
+  tv(s->xk_T, s->ld); tv(s->xh_T, s->ld); tv(s->rhs_T, std::max(s->ld, s->ldq));
+  vec(s->rpart, s->grid_r * (kRedY + 1));
+  vec(s->xpart, s->grid_s * (kRedX + 1));
+  vec(s->zpart, s->grid_z);
+  vec(s->red, 2 * s->ld + kScal);
+  s->cpart.alloc((size_t)s->cplan.slabs * 2 * s->ld * sizeof(double));
+  const int64_t hrows = std::max<int64_t>(s->prm.max_iter, 1) + 1;
+  vec(s->hist, hrows * 8);
+  s->ctl.alloc(sizeof(Ctl));
+  Ctl c{};
+  c.status = GF_STATUS_RUNNING;
+  c.k = 0; c.iterations = 0; c.last_good = -1;
+  c.rho = st_in->rho0; c.rho_prev = st_in->rho0; c.ratio = 1.0; c.final_rho = st_in->rho0;
+  c.r_pri = INFINITY; c.r_dual = INFINITY;
+  GF_CUDA(cudaMemcpyAsync(s->ctl.p, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+  GF_CUDA(cudaMallocHost(&s->pinned, sizeof(Ctl)));
+  GF_CUDA(cudaEventCreate(&s->ev_a));
+  GF_CUDA(cudaEventCreate(&s->ev_b));
+  s->warm_x = x0 != nullptr;
+  if (s->dtype == GF_F32) solver_init<float>(s.get(), x0, nu0, st_in->rho0, st);
+  else solver_init<double>(s.get(), x0, nu0, st_in->rho0, st);
+  // objective of the all-zero half iterate (reported when iteration 0 is degenerate)
+  {
+    DBuf z(std::max(n, m1) * sizeof(double));
+    GF_CUDA(cudaMemsetAsync(z.p, 0, z.bytes, st));
+    const double obj0 = evaluate(s->f.view, s->m, z.as<double>(), st) + evaluate(s->g.view, n, z.as<double>(), st);
+    GF_CUDA(cudaMemcpyAsync(&s->ctl.as<Ctl>()->objective, &obj0, sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  read_ctl(s.get(), st);
+  return s.release();
+}
+
+void solver_run(gf_solver* s, int64_t steps, gf_solver_state* out, cudaStream_t st) {
+  const int64_t last_step = s->prm.max_iter;  // step max_iter is the final projection check
+  int64_t budget = steps > 0 ? steps : INT64_MAX;
+  int64_t chunk = 1;
+  read_ctl(s, st);
+  while (s->host.status == GF_STATUS_RUNNING && s->next_step <= last_step && budget > 0) {
+    const int64_t nlaunch = std::min({chunk, budget, last_step - s->next_step + 1});
+    GF_CUDA(cudaEventRecord(s->ev_a, st));
+    for (int64_t i = 0; i < nlaunch; ++i) {
+      if (s->dtype == GF_F32) launch_step<float>(s, s->next_step, st);
+      else launch_step<double>(s, s->next_step, st);
+      ++s->next_step;
+    }
+    GF_CUDA(cudaEventRecord(s->ev_b, st));
+    budget -= nlaunch;
+    read_ctl(s, st);
+    s->collect();
+    float ms = 0.f;
+    GF_CUDA(cudaEventElapsedTime(&ms, s->ev_a, s->ev_b));
+    s->elapsed_ms += ms;
+    chunk = std::min<int64_t>(chunk * 2, 32);
+  }
+  fill_state(s, out);
+}
+
+void solver_history(gf_solver* s, int64_t count, double* out, cudaStream_t st) {
+  std::vector<double> h(std::max<int64_t>(count, 1) * 8);
+  if (count > 0) {
+    GF_CUDA(cudaMemcpyAsync(h.data(), s->hist.p, count * 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    GF_CUDA(cudaStreamSynchronize(st));
+  }
+  for (int64_t k = 0; k < count; ++k)
+    for (int c = 0; c < 6; ++c) out[k * 6 + c] = h[k * 8 + c];
+}
+
+void solver_snapshot(gf_solver* s, double* x_hat, double* y_hat, double* xt, double* yt, double* xhh, double* yhh,
+                     cudaStream_t st) {
+  DBuf bx(std::max<int64_t>(s->n, 1) * sizeof(double)), by(std::max<int64_t>(s->m, 1) * sizeof(double));
+  snapshot_kernel<<<64, 256, 0, st>>>(s->ctl.as<Ctl>(), s->n, s->m, s->xh2.as<double>(), s->yh2.as<double>(),
+                                      s->S->e.as<double>(), s->S->d.as<double>(), bx.as<double>(), by.as<double>());
+  GF_CHECK_LAUNCH();
+  copy_out(x_hat, s->xk.as<double>(), s->n, st);
+  copy_out(y_hat, s->yk.as<double>(), s->m, st);
+  copy_out(xt, s->xt.as<double>(), s->n, st);
+  copy_out(yt, s->yt.as<double>(), s->m, st);
+  copy_out(xhh, bx.as<double>(), s->n, st);
+  copy_out(yhh, by.as<double>(), s->m, st);
+  GF_CUDA(cudaStreamSynchronize(st));
+}
+
+void solver_result(gf_solver* s, double* x, double* y, double* mu, double* nu, gf_solver_state* out,
+                   cudaStream_t st) {
+  read_ctl(s, st);
+  DBuf bx(std::max<int64_t>(s->n, 1) * sizeof(double)), bm(std::max<int64_t>(s->n, 1) * sizeof(double));
+  DBuf by(std::max<int64_t>(s->m, 1) * sizeof(double)), bn(std::max<int64_t>(s->m, 1) * sizeof(double));
+  result_kernel<<<64, 256, 0, st>>>(s->ctl.as<Ctl>(), s->n, s->m, s->xh2.as<double>(), s->muh2.as<double>(),
+                                    s->yh2.as<double>(), s->nuh2.as<double>(), s->S->e.as<double>(),
+                                    s->S->d.as<double>(), bx.as<double>(), bm.as<double>(), by.as<double>(),
+                                    bn.as<double>());
+  GF_CHECK_LAUNCH();
+  if (x) copy_out(x, bx.as<double>(), s->n, st);
+  if (mu) copy_out(mu, bm.as<double>(), s->n, st);
+  if (y) copy_out(y, by.as<double>(), s->m, st);
+  if (nu) copy_out(nu, bn.as<double>(), s->m, st);
+  GF_CUDA(cudaStreamSynchronize(st));
+  fill_state(s, out);
+}
+
+double solver_elapsed(gf_solver* s) { return s->elapsed_ms; }
+
+void solver_stats(gf_solver* s, int64_t* launches, double* kernel_ms, int64_t* kernel_count) {
+  if (launches) *launches = s->launches;
+  for (int i = 0; i < 8; ++i) {
+    if (kernel_ms) kernel_ms[i] = s->kms[i];
+    if (kernel_count) kernel_count[i] = s->kcount[i];
+  }
+}
+
+void solver_profile(gf_solver* s, int enable) {
+  s->profile = enable != 0;
+  for (int i = 0; i < 8; ++i) { s->kms[i] = 0.0; s->kcount[i] = 0; }
+}
+
+void solver_free(gf_solver* s) { delete s; }
