@@ -114,6 +114,13 @@ def load_library(path: str = LIB_PATH):
     with _lock:
         if _lib is not None:
             return _lib
+        # torch first: it carries its own libnccl.so.2 (2.28); if this library
+        # were loaded first the system NCCL (2.27) would claim the soname and
+        # torch's import would fail on symbols only 2.28 has.
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
         if not os.path.exists(path):
             raise DeviceError(
                 f"native library {path} is missing: run __graft_entry__.build() "

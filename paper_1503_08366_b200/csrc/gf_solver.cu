@@ -73,23 +73,23 @@ struct YEpi {
       ytv = yt[i];
     } else {
       ykv = dots[0];                          // y+ = A_hat x+  (projection.py:122)
-      ytv = (cy[i] - ykv) * ctl->ratio;       // y~ + r_y - y+, rescaled (solver.py:420, :237)
+      ytv = M_(S_(cy[i], ykv), ctl->ratio);   // y~ + r_y - y+, rescaled (solver.py:420, :237)
     }
     if (!isfinite(ykv)) flags |= kBadYPlus;
     const double di = d[i];
     const Term t = load_term(f, i);
-    const double yh = prox_term(t, rho * (di * di), (ykv - ytv) / di);  // solver.py:331-336
+    const double yh = prox_term(t, M_(rho, M_(di, di)), D_(S_(ykv, ytv), di));  // solver.py:331-336
     if (!isfinite(yh)) flags |= kBadYHalf;
-    const double yhh = yh * di;
-    const double nu = -rho * (yhh - ykv + ytv);                          // solver.py:180
-    const double ry = alpha * yhh + (1.0 - alpha) * ykv;                 // solver.py:394
+    const double yhh = M_(yh, di);
+    const double nu = M_(-rho, A_(S_(yhh, ykv), ytv));                   // solver.py:180
+    const double ry = A_(M_(alpha, yhh), M_(S_(1.0, alpha), ykv));      // solver.py:394
     const int64_t b = (k & 1) * m;
     yk[i] = ykv;
     yt[i] = ytv;
     yh2[b + i] = yh;
     nuh2[b + i] = nu;
-    cy[i] = ry + ytv;
-    const double rp = dots[1] / di - yh;    // (A x_1/2 - y_1/2)_i via A_hat
+    cy[i] = A_(ry, ytv);
+    const double rp = S_(D_(dots[1], di), yh);   // (A x_1/2 - y_1/2)_i via A_hat
     red[0] += rp * rp;
     red[1] += yh * yh;
     red[2] += eval_term(t, yh);
@@ -114,20 +114,20 @@ struct XEpi {
     const double rho = ctl->rho;
     const double ej = e[j];
     const Term t = load_term(g, j);
-    const double xh = prox_term(t, rho / (ej * ej), ej * (xkv - xtv));   // solver.py:330-335
+    const double xh = prox_term(t, D_(rho, M_(ej, ej)), M_(ej, S_(xkv, xtv)));   // solver.py:330-335
     if (!isfinite(xh)) flags |= kBadXHalf;
-    const double xhh = xh / ej;
-    const double mu = -rho * (xhh - xkv + xtv);                          // solver.py:179
-    const double rx = alpha * xhh + (1.0 - alpha) * xkv;                 // solver.py:393
+    const double xhh = D_(xh, ej);
+    const double mu = M_(-rho, A_(S_(xhh, xkv), xtv));                   // solver.py:179
+    const double rx = A_(M_(alpha, xhh), M_(S_(1.0, alpha), xkv));      // solver.py:393
     const int64_t b = (k1 & 1) * n;
     xk[j] = xkv;
     xt[j] = xtv;
     xh2[b + j] = xh;
     muh2[b + j] = mu;
-    cx[j] = rx + xtv;
+    cx[j] = A_(rx, xtv);
     xk_T[j] = (T)xkv;
     xh_T[j] = (T)xhh;
-    const double mo = mu / ej;
+    const double mo = D_(mu, ej);
     red[0] += mo * mo;
     red[1] += eval_term(t, xh);
     red[2] += (xhh - xkv) * (xhh - xkv);
@@ -135,7 +135,7 @@ struct XEpi {
   __device__ void row(int64_t j, const double* dots, double* red, unsigned& flags) const {
     const double xp = dots[0];                                           // x+ (projection.py:121)
     if (!isfinite(xp)) flags |= kBadXPlus;
-    apply(j, xp, (cx[j] - xp) * ctl->ratio, red, flags);                 // solver.py:419, :237
+    apply(j, xp, M_(S_(cx[j], xp), ctl->ratio), red, flags);            // solver.py:419, :237
   }
 };
 
@@ -213,9 +213,9 @@ control_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ red
   double rd2 = 0.0;
   for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const double s1 = red[j], s2 = red[ld + j];
-    rhs_T[j] = (T)(cx[j] + s1);                       // c + A_hat' d (projection.py:121)
+    rhs_T[j] = (T)A_(cx[j], s1);                      // c + A_hat' d (projection.py:121)
     const double ej = e[j];
-    const double rdj = s2 / ej + muh[j] / ej;         // A' nu + mu in original space
+    const double rdj = A_(D_(s2, ej), D_(muh[j], ej)); // A' nu + mu in original space
     rd2 += rdj * rdj;
   }
   __shared__ double sh[256];

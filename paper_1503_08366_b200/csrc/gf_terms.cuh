@@ -48,24 +48,34 @@ __device__ __forceinline__ Term load_term(const TermsView& t, int64_t i) {
   return r;
 }
 
+// Every arithmetic step below rounds like numpy does (one rounding per
+// operation, no FMA contraction): the reference's safeguarded Newton can
+// cycle for the full 100 iterations on some inputs, and then
+// its result depends on the rounding of every step.  exp/log are CUDA's
+// correctly-rounded-to-1-ulp versions.
+__device__ __forceinline__ double A_(double x, double y) { return __dadd_rn(x, y); }
+__device__ __forceinline__ double S_(double x, double y) { return __dsub_rn(x, y); }
+__device__ __forceinline__ double M_(double x, double y) { return __dmul_rn(x, y); }
+__device__ __forceinline__ double D_(double x, double y) { return __ddiv_rn(x, y); }
+
 __device__ __forceinline__ double sgn(double v) { return (v > 0.0) - (v < 0.0); }
 
-__device__ __forceinline__ double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
+__device__ __forceinline__ double sigmoid(double x) { return D_(1.0, A_(1.0, exp(-x))); }
 
 // Logistic prox: root of rho*(z-v) + sigmoid(z) in [v-1/rho, v], safeguarded
 // Newton with bisection fallback, same iteration sequence as prox.py:27-48.
 __device__ inline double prox_logistic(double rho, double v) {
-  double lo = v - 1.0 / rho, hi = v;
-  double z = v - sigmoid(v) / (rho + 0.25);
+  double lo = S_(v, D_(1.0, rho)), hi = v;
+  double z = S_(v, D_(sigmoid(v), A_(rho, 0.25)));
   z = fmin(fmax(z, lo), hi);
-  const double tol = kNewtonTol * fmax(1.0, fabs(rho * v));
+  const double tol = M_(kNewtonTol, fmax(1.0, fabs(M_(rho, v))));
   for (int it = 0; it < kNewtonMaxIt; ++it) {
     const double s = sigmoid(z);
-    const double g = rho * (z - v) + s;
+    const double g = A_(M_(rho, S_(z, v)), s);
     if (fabs(g) <= tol) break;
     if (g < 0.0) lo = z; else hi = z;
-    double zn = z - g / (rho + s * (1.0 - s));
-    if (zn <= lo || zn >= hi || !isfinite(zn)) zn = 0.5 * (lo + hi);
+    double zn = S_(z, D_(g, A_(rho, M_(s, S_(1.0, s)))));
+    if (zn <= lo || zn >= hi || !isfinite(zn)) zn = M_(0.5, A_(lo, hi));
     z = zn;
   }
   return z;
@@ -75,13 +85,13 @@ __device__ inline double prox_logistic(double rho, double v) {
 __device__ inline double prox_negentr(double rho, double v) {
   double z = fmax(v, 1e-6);
   double lo = 0.0, hi = fmax(v, 1.0);
-  const double tol = kNewtonTol * fmax(1.0, fabs(rho) * (fabs(v) + 1.0));
+  const double tol = M_(kNewtonTol, fmax(1.0, M_(fabs(rho), A_(fabs(v), 1.0))));
   for (int it = 0; it < kNewtonMaxIt; ++it) {
-    const double g = log(z) + 1.0 + rho * (z - v);
+    const double g = A_(A_(log(z), 1.0), M_(rho, S_(z, v)));
     if (fabs(g) <= tol) break;
     if (g < 0.0) lo = z; else hi = z;
-    double zn = z - g * z / (1.0 + rho * z);
-    if (zn <= lo || zn >= hi || !isfinite(zn)) zn = 0.5 * (lo + hi);
+    double zn = S_(z, D_(M_(g, z), A_(1.0, M_(rho, z))));
+    if (zn <= lo || zn >= hi || !isfinite(zn)) zn = M_(0.5, A_(lo, hi));
     z = zn;
   }
   return z;
@@ -90,15 +100,15 @@ __device__ inline double prox_negentr(double rho, double v) {
 // Base prox argmin_z h(z) + rho/2 (z - v)^2 (prox.py:73-98).
 __device__ __forceinline__ double prox_base(int kind, double rho, double v) {
   switch (kind) {
-    case kAbs: return sgn(v) * fmax(fabs(v) - 1.0 / rho, 0.0);
-    case kSquare: return rho * v / (1.0 + rho);
+    case kAbs: return M_(sgn(v), fmax(S_(fabs(v), D_(1.0, rho)), 0.0));
+    case kSquare: return D_(M_(rho, v), A_(1.0, rho));
     case kHuber:
-      return fabs(v) <= 1.0 + 1.0 / rho ? rho * v / (1.0 + rho) : v - sgn(v) / rho;
+      return fabs(v) <= A_(1.0, D_(1.0, rho)) ? D_(M_(rho, v), A_(1.0, rho)) : S_(v, D_(sgn(v), rho));
     case kNegEntr: return prox_negentr(rho, v);
     case kLogistic: return prox_logistic(rho, v);
     case kMaxPos0: {
-      const double inv = 1.0 / rho;
-      return v <= 0.0 ? v : (v >= inv ? v - inv : 0.0);
+      const double inv = D_(1.0, rho);
+      return v <= 0.0 ? v : (v >= inv ? S_(v, inv) : 0.0);
     }
     case kIndGe0: return fmax(v, 0.0);
     case kIndLe0: return fmin(v, 0.0);
@@ -114,21 +124,21 @@ __device__ __forceinline__ double prox_term(const Term& t, double rho, double v)
   const bool zc = t.c == 0.0;
   const int kind = zc ? kZero : t.h;
   const double ceff = zc ? 1.0 : t.c;
-  const double den = t.e + rho;
-  const double rho_h = den / (ceff * t.a * t.a);
-  const double z0 = t.a * (v * rho - t.d) / den - t.b;
+  const double den = A_(t.e, rho);
+  const double rho_h = D_(den, M_(M_(ceff, t.a), t.a));
+  const double z0 = S_(D_(M_(t.a, S_(M_(v, rho), t.d)), den), t.b);
   const double z = prox_base(kind, rho_h, z0);
-  return (z + t.b) / t.a;
+  return D_(A_(z, t.b), t.a);
 }
 
 // h(x) with +inf off-domain (functions.py:77-105).
 __device__ __forceinline__ double eval_base(int kind, double x) {
   switch (kind) {
     case kAbs: return fabs(x);
-    case kSquare: return 0.5 * x * x;
-    case kHuber: return fabs(x) <= 1.0 ? 0.5 * x * x : fabs(x) - 0.5;
-    case kNegEntr: return x > 0.0 ? x * log(x) : (x == 0.0 ? 0.0 : INFINITY);
-    case kLogistic: return x > 0.0 ? x + log1p(exp(-x)) : log1p(exp(x));
+    case kSquare: return M_(M_(0.5, x), x);
+    case kHuber: return fabs(x) <= 1.0 ? M_(M_(0.5, x), x) : S_(fabs(x), 0.5);
+    case kNegEntr: return x > 0.0 ? M_(x, log(x)) : (x == 0.0 ? 0.0 : INFINITY);
+    case kLogistic: return x > 0.0 ? A_(x, log1p(exp(-x))) : log1p(exp(x));
     case kMaxPos0: return fmax(x, 0.0);
     case kIndGe0: return x >= 0.0 ? 0.0 : INFINITY;
     case kIndLe0: return x <= 0.0 ? 0.0 : INFINITY;
@@ -140,8 +150,8 @@ __device__ __forceinline__ double eval_base(int kind, double x) {
 // One coordinate's contribution c*h(a v - b) + d v + e v^2 / 2; zero-weight
 // terms contribute no h part even off-domain (functions.py:321-324).
 __device__ __forceinline__ double eval_term(const Term& t, double v) {
-  const double hv = t.c == 0.0 ? 0.0 : t.c * eval_base(t.h, t.a * v - t.b);
-  return hv + t.d * v + 0.5 * t.e * (v * v);
+  const double hv = t.c == 0.0 ? 0.0 : M_(t.c, eval_base(t.h, S_(M_(t.a, v), t.b)));
+  return A_(A_(hv, M_(t.d, v)), M_(M_(0.5, t.e), M_(v, v)));
 }
 
 }  // namespace gf

@@ -121,9 +121,19 @@ def test_projection_closed_forms():
     np.testing.assert_allclose(P0.gram, np.eye(3))
 
 
+# Logistic with adaptive rho: the reference's safeguarded Newton (prox.py:27-48)
+# does not converge for some rows (it 2-cycles until the 100-iteration cap), so
+# its output there is a discontinuous function of ulp-level changes of rho*d_i^2.
+# Our D differs from the reference's by ~1 ulp (different summation order in the
+# Sinkhorn sweeps), which flips such a row at iteration 1 of logistic_2000x200
+# (row 1520).  For these cases parity is checked against the oracle run with the
+# GPU's own scaling (same D, E): that isolates the iteration from the ulp-level
+# equilibration difference (tools/debug_logistic2.py shows the oracle then
+# reproduces the GPU value exactly).
+CHAOTIC = ("logistic_2000x200", "logistic_4000x400_prefix")
 SOLVE_FP64 = [n for n in _cases.solve_case_names()
               if not n.endswith("_r32") and "indirect" not in n and "wide" not in n
-              and n not in ("entropy_max_60x300", "portfolio_20x300")]
+              and n not in ("entropy_max_60x300", "portfolio_20x300") and n not in CHAOTIC]
 
 
 @pytest.mark.parametrize("name", SOLVE_FP64)
@@ -142,14 +152,24 @@ def test_solve_fp64_matches_reference(name):
     assert res.final_rho == pytest.approx(float(fx["final_rho"]), rel=1e-9)
 
 
-def test_solve_trajectory_prefix_logistic():
-    fx = _cases.load("solve_logistic_4000x400_prefix")
+@pytest.mark.parametrize("name", CHAOTIC)
+def test_solve_chaotic_logistic_same_scaling(name):
+    fx = _cases.load("solve_" + name)
     prob = _cases.build_problem(fx)
+    st = _cases.settings_of(fx)
+    setup = gf.prepare(prob)
+    # equilibration itself agrees with the reference to a few ulps
+    np.testing.assert_allclose(setup.scaling.d, fx["d"], rtol=1e-13)
     hist = []
-    gf.solve(prob, gf.SolverSettings(max_iter=200),
-             callback=lambda *a: hist.append(a[1:]))
+    res = gf.solve(prob, gf.SolverSettings(**st), setup=setup, callback=lambda *a: hist.append(a[1:]))
+    ref = orc.solve(prob.A, orc.Terms.of(prob.f), orc.Terms.of(prob.g), st,
+                    setup=orc.prepare(prob.A, st, scaling=(setup.scaling.d, setup.scaling.e)))
     h = np.array(hist)
-    np.testing.assert_allclose(h[:150, :2], fx["history"][:150, :2], rtol=1e-5)
+    k = min(150, len(h))
+    np.testing.assert_allclose(h[:k, :2], ref["history"][:k, :2], rtol=1e-5)
+    if "prefix" not in name:
+        assert res.status.value == ref["status"] and res.iterations == ref["iterations"]
+        assert close(res.x, ref["x"], 1e-5)
 
 
 SOLVE_FP32 = [n for n in _cases.solve_case_names() if n.endswith("_r32")]
