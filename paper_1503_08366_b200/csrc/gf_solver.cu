@@ -27,6 +27,7 @@
 
 #include "gf_internal.h"
 #include "gf_gemv.cuh"
+#include "gf_fused.cuh"
 
 namespace gf {
 
@@ -65,6 +66,12 @@ struct YEpi {
   int warm_x;
   __device__ bool active() const { return ctl->status == GF_STATUS_RUNNING; }
   __device__ void row(int64_t i, const double* dots, double* red, unsigned& flags) const {
+    double w0, w1;
+    row_w(i, dots, red, flags, w0, w1);
+  }
+  // w0 = c_y_i, w1 = nu^_1/2_i: the column-pass weights of this row.
+  __device__ void row_w(int64_t i, const double* dots, double* red, unsigned& flags, double& w0,
+                        double& w1) const {
     const int64_t k = ctl->k;
     const double rho = ctl->rho;
     double ykv, ytv;
@@ -89,6 +96,8 @@ struct YEpi {
     yh2[b + i] = yh;
     nuh2[b + i] = nu;
     cy[i] = A_(ry, ytv);
+    w0 = A_(ry, ytv);
+    w1 = nu;
     const double rp = S_(D_(dots[1], di), yh);   // (A x_1/2 - y_1/2)_i via A_hat
     red[0] += rp * rp;
     red[1] += yh * yh;
@@ -382,6 +391,7 @@ struct gf_solver {
   DBuf rpart, cpart, red, zpart, xpart;
   int64_t grid_r = 1, grid_s = 1, grid_z = 1;
   ColPlan cplan;
+  FusedPlan fplan;
   int warm_x = 0;
   int64_t next_step = 0;  // step k = [S(k-1)], R(k), C(k), Z(k)
   Ctl host{};
@@ -403,7 +413,7 @@ struct gf_solver {
   }
   // Kernel classes: 0 S (Ginv GEMV + x side), 1 R (row pass + y side),
   // 2 C (column pass), 3 column-slab reduce, 4 y scalars, 5 controller,
-  // 6 NCCL all-reduce.
+  // 6 NCCL all-reduce, 7 fused row+column pass (replaces 1 and 2).
   void mark(int cls, cudaStream_t st, bool begin) {
     if (!profile) return;
     const size_t idx = ev_marks.size() * 2 + (begin ? 0 : 1);
@@ -440,6 +450,45 @@ static YEpi<T> make_yepi(gf_solver* s) {
   return y;
 }
 
+template <typename T, int NV>
+static void fused_attr(size_t smem) {
+  GF_CUDA(cudaFuncSetAttribute(fused_rowcol_kernel<T, NV, YEpi<T>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+}
+
+template <typename T>
+static void fused_prepare(gf_solver* s) {
+  switch (s->fplan.nv) {
+    case 1: fused_attr<T, 1>(s->fplan.smem); break;
+    case 2: fused_attr<T, 2>(s->fplan.smem); break;
+    case 3: fused_attr<T, 3>(s->fplan.smem); break;
+    case 4: fused_attr<T, 4>(s->fplan.smem); break;
+    case 5: fused_attr<T, 5>(s->fplan.smem); break;
+    default: fused_attr<T, 6>(s->fplan.smem); break;
+  }
+}
+
+template <typename T, int NV>
+static void fused_launch_nv(gf_solver* s, cudaStream_t st) {
+  const FusedPlan& p = s->fplan;
+  fused_rowcol_kernel<T, NV, YEpi<T>><<<p.grid, kFusedThreads, p.smem, st>>>(
+      (const T*)s->S->A->data, s->m, s->ld, s->xk_T.as<T>(), s->xh_T.as<T>(), make_yepi<T>(s), p.nslot, p.tr,
+      s->rpart.as<double>(), s->cpart.as<double>());
+  GF_CHECK_LAUNCH();
+}
+
+template <typename T>
+static void launch_fused(gf_solver* s, cudaStream_t st) {
+  switch (s->fplan.nv) {
+    case 1: fused_launch_nv<T, 1>(s, st); break;
+    case 2: fused_launch_nv<T, 2>(s, st); break;
+    case 3: fused_launch_nv<T, 3>(s, st); break;
+    case 4: fused_launch_nv<T, 4>(s, st); break;
+    case 5: fused_launch_nv<T, 5>(s, st); break;
+    default: fused_launch_nv<T, 6>(s, st); break;
+  }
+}
+
 template <typename T>
 static XEpi<T> make_xepi(gf_solver* s) {
   XEpi<T> x;
@@ -467,27 +516,40 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
     s->launches += 1;
   }
   if (s->m > 0) {
-    s->mark(1, st, true);
-    rowgemv_kernel<T, 2, YEpi<T>><<<(unsigned)s->grid_r, kRowThreads, 0, st>>>(
-        (const T*)A->data, s->m, s->ld, s->xk_T.as<T>(), s->xh_T.as<T>(), make_yepi<T>(s), s->rpart.as<double>());
-    GF_CHECK_LAUNCH();
-    s->mark(1, st, false);
-    s->mark(2, st, true);
-    colgemv_kernel<T, 2, false><<<dim3((unsigned)s->cplan.col_blocks, (unsigned)s->cplan.slabs), kColThreads, 0, st>>>(
-        (const T*)A->data, s->m, s->ld, s->cy.as<double>(), s->nuh2.as<double>() + (k & 1) * s->m,
-        s->cplan.rows_per_slab, s->cpart.as<double>(), &ctl->status);
-    GF_CHECK_LAUNCH();
-    s->mark(2, st, false);
+    int64_t slabs, nrpart;
+    if (s->fplan.ok) {   // one pass over A_hat: row pass + y side + column pass
+      s->mark(7, st, true);
+      launch_fused<T>(s, st);
+      s->mark(7, st, false);
+      slabs = s->fplan.grid;
+      nrpart = s->fplan.grid;
+      s->launches += 1;
+    } else {             // two passes: row pass (+ y side), then column pass
+      s->mark(1, st, true);
+      rowgemv_kernel<T, 2, YEpi<T>><<<(unsigned)s->grid_r, kRowThreads, 0, st>>>(
+          (const T*)A->data, s->m, s->ld, s->xk_T.as<T>(), s->xh_T.as<T>(), make_yepi<T>(s), s->rpart.as<double>());
+      GF_CHECK_LAUNCH();
+      s->mark(1, st, false);
+      s->mark(2, st, true);
+      colgemv_kernel<T, 2, false><<<dim3((unsigned)s->cplan.col_blocks, (unsigned)s->cplan.slabs), kColThreads, 0, st>>>(
+          (const T*)A->data, s->m, s->ld, s->cy.as<double>(), s->nuh2.as<double>() + (k & 1) * s->m,
+          s->cplan.rows_per_slab, s->cpart.as<double>(), &ctl->status);
+      GF_CHECK_LAUNCH();
+      s->mark(2, st, false);
+      slabs = s->cplan.slabs;
+      nrpart = s->grid_r;
+      s->launches += 2;
+    }
     s->mark(3, st, true);
     colreduce_kernel<<<dim3((unsigned)ceil_div(s->ld, 32), 2), dim3(32, 8), 0, st>>>(
-        s->cpart.as<double>(), s->cplan.slabs, s->ld, 2, s->red.as<double>(), &ctl->status);
+        s->cpart.as<double>(), slabs, s->ld, 2, s->red.as<double>(), &ctl->status);
     GF_CHECK_LAUNCH();
     s->mark(3, st, false);
     s->mark(4, st, true);
-    y_scalars_kernel<<<1, 256, 0, st>>>(s->rpart.as<double>(), s->grid_r, s->red.as<double>() + 2 * s->ld, ctl);
+    y_scalars_kernel<<<1, 256, 0, st>>>(s->rpart.as<double>(), nrpart, s->red.as<double>() + 2 * s->ld, ctl);
     GF_CHECK_LAUNCH();
     s->mark(4, st, false);
-    s->launches += 4;
+    s->launches += 2;
   } else {
     GF_CUDA(cudaMemsetAsync(s->red.p, 0, (2 * s->ld + kScal) * sizeof(double), st));
   }
@@ -584,11 +646,24 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
   vec(s->yk, m1); vec(s->yt, m1); vec(s->cy, m1); vec(s->yh2, 2 * m1); vec(s->nuh2, 2 * m1);
   auto tv = [&](DBuf& b, int64_t len) { b.alloc(len * es); GF_CUDA(cudaMemsetAsync(b.p, 0, b.bytes, st)); };
   tv(s->xk_T, s->ld); tv(s->xh_T, s->ld); tv(s->rhs_T, std::max(s->ld, s->ldq));
-  vec(s->rpart, s->grid_r * (kRedY + 1));
+  {
+    int dev = 0, optin = 0;
+    GF_CUDA(cudaGetDevice(&dev));
+    GF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    s->fplan = plan_fused(s->m, s->ld, (int)es, sms, (size_t)optin);
+    const char* env = getenv("GF_DISABLE_FUSED");
+    if (env && env[0] == '1') s->fplan.ok = false;
+    if (s->fplan.ok) {
+      if (s->dtype == GF_F32) fused_prepare<float>(s.get());
+      else fused_prepare<double>(s.get());
+    }
+  }
+  const int64_t nslab = std::max<int64_t>(s->cplan.slabs, s->fplan.ok ? s->fplan.grid : 1);
+  vec(s->rpart, std::max<int64_t>(s->grid_r, s->fplan.ok ? s->fplan.grid : 1) * (kRedY + 1));
   vec(s->xpart, s->grid_s * (kRedX + 1));
   vec(s->zpart, s->grid_z);
   vec(s->red, 2 * s->ld + kScal);
-  s->cpart.alloc((size_t)s->cplan.slabs * 2 * s->ld * sizeof(double));
+  s->cpart.alloc((size_t)nslab * 2 * s->ld * sizeof(double));
   const int64_t hrows = std::max<int64_t>(s->prm.max_iter, 1) + 1;
   vec(s->hist, hrows * 8);
   s->ctl.alloc(sizeof(Ctl));
