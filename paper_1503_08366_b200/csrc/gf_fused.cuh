@@ -120,16 +120,35 @@ inline FusedPlan plan_fused(int64_t m, int64_t ld, int esize, int sms, size_t sm
   const size_t row_bytes = (size_t)ld * esize;
   const size_t budget = smem_max > 8192 ? smem_max - 8192 : 0;
   p.nslot = (int)std::min<size_t>(kMaxSlots, budget / row_bytes);
-  p.tr = std::min(kMaxTR, p.nslot / 2);
+  // two resident groups (row pass of t, column pass of t-1) + TMA prefetch
+  p.tr = std::min(kMaxTR, std::max(1, (p.nslot - 2) / 2));
+  if (2 * p.tr + 1 > p.nslot) p.tr = 0;
   p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, m));
   p.smem = (size_t)p.nslot * row_bytes;
   p.ok = p.nv >= 1 && p.nv <= 6 && p.nslot >= 2 && p.tr >= 1 && m > 0;
   return p;
 }
 
-// Epi must provide row_w(i, dots, red, flags, w0, w1) (YEpi does).
+// Warp roles: warps 0..15 stream the row and column passes; warp 16 is the
+// epilogue warp (lane rr handles row rr of a group).  Software pipeline over
+// groups of TR rows, two CTA barriers per group:
+//
+//   iteration t:  compute warps   R(t): dots of group t -> red_s
+//                 epilogue warp   (inputs of group t were prefetched in t-1)
+//   --- barrier A ---
+//                 epilogue warp   reduce red_s, y-side epilogue of group t
+//                                 -> w_s[t&1]; prefetch inputs of group t+1
+//                 compute warps   C(t-1): column pass of group t-1 with
+//                                 w_s[(t-1)&1] (overlaps the epilogue)
+//   --- barrier B ---
+//                 thread 0        refill the slots of group t-1 (rows NSLOT ahead)
+//
+// so the serial epilogue latency hides behind a column pass, and the ring
+// holds two groups plus NSLOT - 2*TR rows of TMA prefetch.
+constexpr int kFusedCTA = kFusedThreads + kWarp;
+
 template <typename T, int NV, class Epi>
-__global__ void __launch_bounds__(kFusedThreads, 1)
+__global__ void __launch_bounds__(kFusedCTA, 1)
 fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* __restrict__ x0,
                     const T* __restrict__ x1, Epi epi, int nslot, int tr, double* __restrict__ rpart,
                     double* __restrict__ cpart) {
@@ -139,17 +158,17 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxSlots];
   __shared__ double red_s[kFusedWarps][2 * kMaxTR];
-  __shared__ T w_s[kMaxTR][2];
-  __shared__ double epi_s[kMaxTR][NR + 1];
+  __shared__ T w_s[2][kMaxTR][2];
 
   if (!epi.active()) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool is_epi = warp == kFusedWarps;
   const int64_t nvec = ld / VN;
   const size_t row_bytes = (size_t)ld * sizeof(T);
-  // contiguous, balanced row range of this CTA
-  const int64_t r0 = rows * blockIdx.x / gridDim.x;
+  const int64_t r0 = rows * blockIdx.x / gridDim.x;   // contiguous, balanced row range
   const int64_t r1 = rows * (blockIdx.x + 1) / gridDim.x;
   const int64_t nrows = r1 - r0;
+  const int64_t ngroups = (nrows + tr - 1) / tr;
 
   if (tid == 0) {
     for (int s = 0; s < nslot; ++s) mbar_init(&full[s], 1);
@@ -164,102 +183,108 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
       bulk_g2s(smem_raw + (size_t)s * row_bytes, A + (r0 + s) * ld, (unsigned)row_bytes, &full[s], pol);
     }
   }
-  // x^ and x^_1/2 for this thread's columns stay in registers
   V xa[NV], xb[NV], ca[NV], cb[NV];
-  const V* xv0 = reinterpret_cast<const V*>(x0);
-  const V* xv1 = reinterpret_cast<const V*>(x1);
+  if (!is_epi) {
+    const V* xv0 = reinterpret_cast<const V*>(x0);
+    const V* xv1 = reinterpret_cast<const V*>(x1);
 #pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    const int64_t c = tid + (int64_t)v * kFusedThreads;
-    if (c < nvec) {
-      xa[v] = xv0[c];
-      xb[v] = xv1[c];
-    } else {
-      xa[v] = V{};
-      xb[v] = V{};
+    for (int v = 0; v < NV; ++v) {
+      const int64_t c = tid + (int64_t)v * kFusedThreads;
+      xa[v] = c < nvec ? xv0[c] : V{};
+      xb[v] = c < nvec ? xv1[c] : V{};
+      ca[v] = V{};
+      cb[v] = V{};
     }
-    ca[v] = V{};
-    cb[v] = V{};
   }
   double ered[NR > 0 ? NR : 1];
 #pragma unroll
   for (int k = 0; k < (NR > 0 ? NR : 1); ++k) ered[k] = 0.0;
   unsigned eflags = 0;
+  typename Epi::RowIn in_next{};
+  if (is_epi && lane < tr && lane < nrows) in_next = epi.load_in(r0 + lane);
 
-  for (int64_t j0 = 0; j0 < nrows; j0 += tr) {
-    const int g = (int)std::min<int64_t>(tr, nrows - j0);
-    // ---- 1. row pass over the group ----
-    T s0[kMaxTR], s1[kMaxTR];
+  for (int64_t t = 0; t <= ngroups; ++t) {
+    const int64_t j0 = t * tr;
+    const int g = t < ngroups ? (int)min((int64_t)tr, nrows - j0) : 0;
+    if (!is_epi && g > 0) {
+      // ---- R(t): row pass of group t ----
+      T s0[kMaxTR], s1[kMaxTR];
 #pragma unroll
-    for (int rr = 0; rr < kMaxTR; ++rr) { s0[rr] = 0; s1[rr] = 0; }
+      for (int rr = 0; rr < kMaxTR; ++rr) { s0[rr] = 0; s1[rr] = 0; }
 #pragma unroll
-    for (int rr = 0; rr < kMaxTR; ++rr) {
-      if (rr < g) {
-        const int64_t j = j0 + rr;
-        const int slot = (int)(j % nslot);
-        mbar_wait(&full[slot], (unsigned)((j / nslot) & 1));
-        const V* row = reinterpret_cast<const V*>(smem_raw + (size_t)slot * row_bytes);
+      for (int rr = 0; rr < kMaxTR; ++rr) {
+        if (rr < g) {
+          const int64_t j = j0 + rr;
+          const int slot = (int)(j % nslot);
+          mbar_wait(&full[slot], (unsigned)((j / nslot) & 1));
+          const V* row = reinterpret_cast<const V*>(smem_raw + (size_t)slot * row_bytes);
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const int64_t c = tid + (int64_t)v * kFusedThreads;
-          if (c < nvec) {
-            const V a = row[c];
-            s0[rr] = vdot(a, xa[v], s0[rr]);
-            s1[rr] = vdot(a, xb[v], s1[rr]);
+          for (int v = 0; v < NV; ++v) {
+            const int64_t c = tid + (int64_t)v * kFusedThreads;
+            if (c < nvec) {
+              const V a = row[c];
+              s0[rr] = vdot(a, xa[v], s0[rr]);
+              s1[rr] = vdot(a, xb[v], s1[rr]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < kMaxTR; ++rr) {
+        if (rr < g) {
+          const T a = warp_sum(s0[rr]);
+          const T b = warp_sum(s1[rr]);
+          if (lane == 0) {
+            red_s[warp][2 * rr] = (double)a;
+            red_s[warp][2 * rr + 1] = (double)b;
           }
         }
       }
     }
-    // ---- 2. reduce the 2*g dots over the CTA ----
-#pragma unroll
-    for (int rr = 0; rr < kMaxTR; ++rr) {
-      if (rr < g) {
-        const T a = warp_sum(s0[rr]);
-        const T b = warp_sum(s1[rr]);
-        if (lane == 0) {
-          red_s[warp][2 * rr] = (double)a;
-          red_s[warp][2 * rr + 1] = (double)b;
+    __syncthreads();  // A
+    if (is_epi) {
+      if (lane < g) {   // ---- epilogue of group t ----
+        const int rr = lane;
+        double dots[2] = {0.0, 0.0};
+        for (int w = 0; w < kFusedWarps; ++w) {
+          dots[0] += red_s[w][2 * rr];
+          dots[1] += red_s[w][2 * rr + 1];
         }
+        double w0, w1;
+        epi.finish(r0 + j0 + rr, in_next, dots, ered, eflags, w0, w1);
+        w_s[t & 1][rr][0] = (T)w0;
+        w_s[t & 1][rr][1] = (T)w1;
       }
-    }
-    __syncthreads();
-    // ---- 3. y-side epilogue, one thread per row (warp rr, lane 0) ----
-    if (lane == 0 && warp < g) {
-      const int rr = warp;
-      double dots[2] = {0.0, 0.0};
-      for (int w = 0; w < kFusedWarps; ++w) {
-        dots[0] += red_s[w][2 * rr];
-        dots[1] += red_s[w][2 * rr + 1];
-      }
-      double w0, w1;
-      epi.row_w(r0 + j0 + rr, dots, ered, eflags, w0, w1);
-      w_s[rr][0] = (T)w0;
-      w_s[rr][1] = (T)w1;
-    }
-    __syncthreads();
-    // ---- 4. column pass: A' [c_y, nu^] over the same staged rows ----
+      const int64_t jn = j0 + tr + lane;   // prefetch the inputs of group t+1
+      if (lane < tr && jn < nrows) in_next = epi.load_in(r0 + jn);
+    } else if (t >= 1) {
+      // ---- C(t-1): column pass of the previous group ----
+      const int64_t jp = j0 - tr;
+      const int gp = (int)min((int64_t)tr, nrows - jp);
 #pragma unroll
-    for (int rr = 0; rr < kMaxTR; ++rr) {
-      if (rr < g) {
-        const int slot = (int)((j0 + rr) % nslot);
-        const V* row = reinterpret_cast<const V*>(smem_raw + (size_t)slot * row_bytes);
-        const T w0 = w_s[rr][0], w1 = w_s[rr][1];
+      for (int rr = 0; rr < kMaxTR; ++rr) {
+        if (rr < gp) {
+          const int slot = (int)((jp + rr) % nslot);
+          const V* row = reinterpret_cast<const V*>(smem_raw + (size_t)slot * row_bytes);
+          const T w0 = w_s[(t - 1) & 1][rr][0], w1 = w_s[(t - 1) & 1][rr][1];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const int64_t c = tid + (int64_t)v * kFusedThreads;
-          if (c < nvec) {
-            const V a = row[c];
-            vaxpy(ca[v], a, w0);
-            vaxpy(cb[v], a, w1);
+          for (int v = 0; v < NV; ++v) {
+            const int64_t c = tid + (int64_t)v * kFusedThreads;
+            if (c < nvec) {
+              const V a = row[c];
+              vaxpy(ca[v], a, w0);
+              vaxpy(cb[v], a, w1);
+            }
           }
         }
       }
     }
-    __syncthreads();
-    // ---- 5. refill the group's slots with the rows nslot ahead ----
-    if (tid == 0) {
-      for (int rr = 0; rr < g; ++rr) {
-        const int64_t jn = j0 + rr + nslot;
+    __syncthreads();  // B
+    if (tid == 0 && t >= 1) {   // refill the slots of group t-1
+      const int64_t jp = j0 - tr;
+      const int gp = (int)min((int64_t)tr, nrows - jp);
+      for (int rr = 0; rr < gp; ++rr) {
+        const int64_t jn = jp + rr + nslot;
         if (jn < nrows) {
           const int slot = (int)(jn % nslot);
           mbar_arrive_expect_tx(&full[slot], (unsigned)row_bytes);
@@ -268,36 +293,27 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
       }
     }
   }
-  // ---- column partials of this CTA (one slab) ----
+  if (!is_epi) {   // column partials of this CTA (one slab)
 #pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    const int64_t c = tid + (int64_t)v * kFusedThreads;
-    if (c < nvec) {
-      double* p0 = cpart + ((int64_t)blockIdx.x * 2) * ld + c * VN;
-      double* p1 = cpart + ((int64_t)blockIdx.x * 2 + 1) * ld + c * VN;
+    for (int v = 0; v < NV; ++v) {
+      const int64_t c = tid + (int64_t)v * kFusedThreads;
+      if (c < nvec) {
+        double* p0 = cpart + ((int64_t)blockIdx.x * 2) * ld + c * VN;
+        double* p1 = cpart + ((int64_t)blockIdx.x * 2 + 1) * ld + c * VN;
 #pragma unroll
-      for (int i = 0; i < VN; ++i) {
-        p0[i] = (double)vget(ca[v], i);
-        p1[i] = (double)vget(cb[v], i);
+        for (int i = 0; i < VN; ++i) {
+          p0[i] = (double)vget(ca[v], i);
+          p1[i] = (double)vget(cb[v], i);
+        }
       }
     }
-  }
-  // ---- epilogue partials (held by warp rr lane 0 threads) ----
-  if (lane == 0 && warp < kMaxTR) {
-    for (int k = 0; k < NR; ++k) epi_s[warp][k] = ered[k];
-    epi_s[warp][NR] = (double)eflags;
-  }
-  __syncthreads();
-  if (tid <= NR) {
-    const int k = tid;
-    if (k < NR) {
-      double s = 0.0;
-      for (int w = 0; w < tr; ++w) s += epi_s[w][k];
-      rpart[blockIdx.x * (NR + 1) + k] = s;
-    } else {
-      unsigned f = 0;
-      for (int w = 0; w < tr; ++w) f |= (unsigned)epi_s[w][NR];
-      rpart[blockIdx.x * (NR + 1) + NR] = (double)f;
+  } else {         // epilogue partials, held by the epilogue warp
+#pragma unroll
+    for (int k = 0; k < NR; ++k) ered[k] = warp_sum(ered[k]);
+    eflags = warp_or(eflags);
+    if (lane == 0) {
+      for (int k = 0; k < NR; ++k) rpart[blockIdx.x * (NR + 1) + k] = ered[k];
+      rpart[blockIdx.x * (NR + 1) + NR] = (double)eflags;
     }
   }
 }

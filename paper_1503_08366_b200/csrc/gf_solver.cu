@@ -69,22 +69,40 @@ struct YEpi {
     double w0, w1;
     row_w(i, dots, red, flags, w0, w1);
   }
+  // Per-row inputs of the epilogue, loadable ahead of the dot products.
+  struct RowIn {
+    double di, cy, yk, yt;
+    Term t;
+  };
+  __device__ RowIn load_in(int64_t i) const {
+    RowIn in;
+    in.di = d[i];
+    in.cy = cy[i];
+    in.yk = yk[i];
+    in.yt = yt[i];
+    in.t = load_term(f, i);
+    return in;
+  }
   // w0 = c_y_i, w1 = nu^_1/2_i: the column-pass weights of this row.
   __device__ void row_w(int64_t i, const double* dots, double* red, unsigned& flags, double& w0,
                         double& w1) const {
+    finish(i, load_in(i), dots, red, flags, w0, w1);
+  }
+  __device__ void finish(int64_t i, const RowIn& in, const double* dots, double* red, unsigned& flags,
+                         double& w0, double& w1) const {
     const int64_t k = ctl->k;
     const double rho = ctl->rho;
     double ykv, ytv;
     if (k == 0) {
-      ykv = warm_x ? dots[0] : yk[i];
-      ytv = yt[i];
+      ykv = warm_x ? dots[0] : in.yk;
+      ytv = in.yt;
     } else {
       ykv = dots[0];                          // y+ = A_hat x+  (projection.py:122)
-      ytv = M_(S_(cy[i], ykv), ctl->ratio);   // y~ + r_y - y+, rescaled (solver.py:420, :237)
+      ytv = M_(S_(in.cy, ykv), ctl->ratio);   // y~ + r_y - y+, rescaled (solver.py:420, :237)
     }
     if (!isfinite(ykv)) flags |= kBadYPlus;
-    const double di = d[i];
-    const Term t = load_term(f, i);
+    const double di = in.di;
+    const Term& t = in.t;
     const double yh = prox_term(t, M_(rho, M_(di, di)), D_(S_(ykv, ytv), di));  // solver.py:331-336
     if (!isfinite(yh)) flags |= kBadYHalf;
     const double yhh = M_(yh, di);
@@ -471,7 +489,7 @@ static void fused_prepare(gf_solver* s) {
 template <typename T, int NV>
 static void fused_launch_nv(gf_solver* s, cudaStream_t st) {
   const FusedPlan& p = s->fplan;
-  fused_rowcol_kernel<T, NV, YEpi<T>><<<p.grid, kFusedThreads, p.smem, st>>>(
+  fused_rowcol_kernel<T, NV, YEpi<T>><<<p.grid, kFusedCTA, p.smem, st>>>(
       (const T*)s->S->A->data, s->m, s->ld, s->xk_T.as<T>(), s->xh_T.as<T>(), make_yepi<T>(s), p.nslot, p.tr,
       s->rpart.as<double>(), s->cpart.as<double>());
   GF_CHECK_LAUNCH();
