@@ -6,24 +6,28 @@
 // projection.py:121-122), and the plain restatement still needs two passes:
 // y+ = A_hat x+ (row pass) and A_hat' [c_y, nu^] (column pass).  But c_y and
 // nu^ of row i depend only on row i's own dot products, so the column pass can
-// consume each row right after the row pass has produced its epilogue -- while
-// the row is still on chip.  One iteration then streams A_hat from HBM once:
+// consume each row once its epilogue is done -- while the row is still on
+// chip.  One iteration then streams A_hat from HBM exactly once.
 //
-//   persistent CTA per SM, contiguous row range; a ring of NSLOT row slots in
-//   shared memory filled by TMA bulk copies (cp.async.bulk, L2 evict_first,
-//   one mbarrier per slot); rows are consumed in groups of TR:
-//     1. row pass    every thread owns fixed 16-byte column vectors (x^ and
-//                    x^_1/2 for them live in registers for the whole kernel)
-//     2. reduce      warp shuffles + one shared-memory stage -> 2 dots per row
-//     3. epilogue    one thread per row (different warps): the full y side of
-//                    the iteration (YEpi: dual step, prox_f, nu^, c_y, partials)
-//     4. column pass the same threads re-read the same columns of the group's
-//                    rows from shared memory and accumulate A' [c_y, nu^] in
-//                    registers
-//     5. release     barrier, then thread 0 refills the group's slots with rows
-//                    NSLOT ahead
-//   At the end each CTA writes its column partials (one "slab" per CTA) and
-//   its epilogue reduction partials; colreduce + y_scalars finish them.
+// Structure: one persistent CTA per SM over a contiguous row range; a ring of
+// NSLOT row slots in shared memory filled by TMA bulk copies (cp.async.bulk,
+// L2 evict_first, one mbarrier per slot).  16 compute warps own fixed 16-byte
+// column vectors (x^ and x^_1/2 for them, and the column accumulators, live in
+// registers for the whole kernel); one epilogue warp runs the y side.  Rows
+// move in groups of TR through a three-stage software pipeline with ONE CTA
+// barrier per group:
+//
+//   iteration t:  compute warps   R(t)   dots of group t        -> red_s[t&1]
+//                                 C(t-2) A' [c_y, nu^] of group t-2 with w_s[t&1]
+//                 epilogue warp   E(t-1) reduce red_s[(t-1)&1]; y side of group
+//                                 t-1 (YEpi::finish) -> w_s[(t-1)&1]; prefetch
+//                                 the per-row inputs of group t
+//   --- barrier ---
+//                 thread 0        refill the slots of group t-2 (rows NSLOT ahead)
+//
+// so the serial per-row epilogue (fp64 prox, divisions, global stores) runs
+// concurrently with a row pass and a column pass instead of between them.
+// Three groups are resident; NSLOT - 3*TR rows are in flight from HBM.
 #pragma once
 
 #include "gf_common.cuh"
@@ -31,10 +35,10 @@
 
 namespace gf {
 
-constexpr int kFusedThreads = 512;
+constexpr int kFusedThreads = 512;                 // compute threads
 constexpr int kFusedWarps = kFusedThreads / kWarp;
+constexpr int kFusedCTA = kFusedThreads + kWarp;   // + the epilogue warp
 constexpr int kMaxSlots = 32;
-constexpr int kMaxTR = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -106,7 +110,7 @@ __device__ __forceinline__ void vaxpy(double2& acc, const double2& a, double w) 
 struct FusedPlan {
   int nv = 0;        // 16-byte vectors per thread per row (template instance)
   int nslot = 0;     // rows resident in shared memory
-  int tr = 0;        // rows per group
+  int tr = 0;        // rows per group (template instance: 1, 2 or 4)
   int grid = 0;      // CTAs (one per SM)
   size_t smem = 0;   // dynamic shared memory bytes
   bool ok = false;
@@ -120,45 +124,31 @@ inline FusedPlan plan_fused(int64_t m, int64_t ld, int esize, int sms, size_t sm
   const size_t row_bytes = (size_t)ld * esize;
   const size_t budget = smem_max > 8192 ? smem_max - 8192 : 0;
   p.nslot = (int)std::min<size_t>(kMaxSlots, budget / row_bytes);
-  // two resident groups (row pass of t, column pass of t-1) + TMA prefetch
-  p.tr = std::min(kMaxTR, std::max(1, (p.nslot - 2) / 2));
-  if (2 * p.tr + 1 > p.nslot) p.tr = 0;
+  // keep >= 2 rows and >= 48 KB of TMA prefetch beyond the three resident groups
+  const int want_pf = std::max<int>(2, (int)ceil_div(48 * 1024, (int64_t)row_bytes));
+  p.tr = 0;
+  for (int tr : {4, 2, 1})
+    if (3 * tr + want_pf <= p.nslot || (tr == 1 && 3 + 1 <= p.nslot)) { p.tr = tr; break; }
   p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, m));
   p.smem = (size_t)p.nslot * row_bytes;
-  p.ok = p.nv >= 1 && p.nv <= 6 && p.nslot >= 2 && p.tr >= 1 && m > 0;
+  p.ok = p.nv >= 1 && p.nv <= 6 && p.tr >= 1 && m > 0;
   return p;
 }
 
-// Warp roles: warps 0..15 stream the row and column passes; warp 16 is the
-// epilogue warp (lane rr handles row rr of a group).  Software pipeline over
-// groups of TR rows, two CTA barriers per group:
-//
-//   iteration t:  compute warps   R(t): dots of group t -> red_s
-//                 epilogue warp   (inputs of group t were prefetched in t-1)
-//   --- barrier A ---
-//                 epilogue warp   reduce red_s, y-side epilogue of group t
-//                                 -> w_s[t&1]; prefetch inputs of group t+1
-//                 compute warps   C(t-1): column pass of group t-1 with
-//                                 w_s[(t-1)&1] (overlaps the epilogue)
-//   --- barrier B ---
-//                 thread 0        refill the slots of group t-1 (rows NSLOT ahead)
-//
-// so the serial epilogue latency hides behind a column pass, and the ring
-// holds two groups plus NSLOT - 2*TR rows of TMA prefetch.
-constexpr int kFusedCTA = kFusedThreads + kWarp;
-
-template <typename T, int NV, class Epi>
+// Epi must provide: NR, active(), begin(), RowIn, load_in(i),
+// finish(i, in, dots, red, flags, w0, w1)   (YEpi in gf_solver.cu does).
+template <typename T, int NV, int TR, class Epi>
 __global__ void __launch_bounds__(kFusedCTA, 1)
 fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* __restrict__ x0,
-                    const T* __restrict__ x1, Epi epi, int nslot, int tr, double* __restrict__ rpart,
+                    const T* __restrict__ x1, Epi epi, int nslot, double* __restrict__ rpart,
                     double* __restrict__ cpart) {
   using V = typename Vec16<T>::type;
   constexpr int VN = Vec16<T>::n;
   constexpr int NR = Epi::NR;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxSlots];
-  __shared__ double red_s[kFusedWarps][2 * kMaxTR];
-  __shared__ T w_s[2][kMaxTR][2];
+  __shared__ double red_s[2][kFusedWarps][2 * TR];
+  __shared__ T w_s[2][TR][2];
 
   if (!epi.active()) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -168,7 +158,7 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
   const int64_t r0 = rows * blockIdx.x / gridDim.x;   // contiguous, balanced row range
   const int64_t r1 = rows * (blockIdx.x + 1) / gridDim.x;
   const int64_t nrows = r1 - r0;
-  const int64_t ngroups = (nrows + tr - 1) / tr;
+  const int64_t ngroups = (nrows + TR - 1) / TR;
 
   if (tid == 0) {
     for (int s = 0; s < nslot; ++s) mbar_init(&full[s], 1);
@@ -183,8 +173,54 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
       bulk_g2s(smem_raw + (size_t)s * row_bytes, A + (r0 + s) * ld, (unsigned)row_bytes, &full[s], pol);
     }
   }
+  if (is_epi) {
+    // ===================== epilogue warp =====================
+    epi.begin();
+    double ered[NR > 0 ? NR : 1];
+#pragma unroll
+    for (int k = 0; k < (NR > 0 ? NR : 1); ++k) ered[k] = 0.0;
+    unsigned eflags = 0;
+    typename Epi::RowIn in{};
+    if (lane < TR && lane < nrows) in = epi.load_in(r0 + lane);
+    for (int64_t t = 0; t < ngroups + 2; ++t) {
+      const int64_t ge = t - 1;   // group whose epilogue runs now
+      if (ge >= 0 && ge < ngroups) {
+        const int g = (int)min((int64_t)TR, nrows - ge * TR);
+        // cross-warp reduction of the 2*TR dots: lanes 0..15 hold one warp each
+        double v[2 * TR];
+#pragma unroll
+        for (int q = 0; q < 2 * TR; ++q) v[q] = lane < kFusedWarps ? red_s[ge & 1][lane][q] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 2 * TR; ++q)
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o, 16);
+        if (lane < g) {
+          double dots[2] = {0.0, 0.0};
+#pragma unroll
+          for (int rr = 0; rr < TR; ++rr)
+            if (rr == lane) { dots[0] = v[2 * rr]; dots[1] = v[2 * rr + 1]; }
+          double w0, w1;
+          epi.finish(r0 + ge * TR + lane, in, dots, ered, eflags, w0, w1);
+          w_s[ge & 1][lane][0] = (T)w0;
+          w_s[ge & 1][lane][1] = (T)w1;
+        }
+        const int64_t jn = (ge + 1) * TR + lane;   // prefetch the inputs of the next group
+        if (lane < TR && jn < nrows) in = epi.load_in(r0 + jn);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < NR; ++k) ered[k] = warp_sum(ered[k]);
+    eflags = warp_or(eflags);
+    if (lane == 0) {
+      for (int k = 0; k < NR; ++k) rpart[blockIdx.x * (NR + 1) + k] = ered[k];
+      rpart[blockIdx.x * (NR + 1) + NR] = (double)eflags;
+    }
+    return;
+  }
+  // ===================== compute warps =====================
   V xa[NV], xb[NV], ca[NV], cb[NV];
-  if (!is_epi) {
+  {
     const V* xv0 = reinterpret_cast<const V*>(x0);
     const V* xv1 = reinterpret_cast<const V*>(x1);
 #pragma unroll
@@ -196,23 +232,15 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
       cb[v] = V{};
     }
   }
-  double ered[NR > 0 ? NR : 1];
+  for (int64_t t = 0; t < ngroups + 2; ++t) {
+    if (t < ngroups) {   // ---- R(t) ----
+      const int64_t j0 = t * TR;
+      const int g = (int)min((int64_t)TR, nrows - j0);
+      T s0[TR], s1[TR];
 #pragma unroll
-  for (int k = 0; k < (NR > 0 ? NR : 1); ++k) ered[k] = 0.0;
-  unsigned eflags = 0;
-  typename Epi::RowIn in_next{};
-  if (is_epi && lane < tr && lane < nrows) in_next = epi.load_in(r0 + lane);
-
-  for (int64_t t = 0; t <= ngroups; ++t) {
-    const int64_t j0 = t * tr;
-    const int g = t < ngroups ? (int)min((int64_t)tr, nrows - j0) : 0;
-    if (!is_epi && g > 0) {
-      // ---- R(t): row pass of group t ----
-      T s0[kMaxTR], s1[kMaxTR];
-#pragma unroll
-      for (int rr = 0; rr < kMaxTR; ++rr) { s0[rr] = 0; s1[rr] = 0; }
-#pragma unroll
-      for (int rr = 0; rr < kMaxTR; ++rr) {
+      for (int rr = 0; rr < TR; ++rr) {
+        s0[rr] = 0;
+        s1[rr] = 0;
         if (rr < g) {
           const int64_t j = j0 + rr;
           const int slot = (int)(j % nslot);
@@ -230,43 +258,24 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
         }
       }
 #pragma unroll
-      for (int rr = 0; rr < kMaxTR; ++rr) {
-        if (rr < g) {
-          const T a = warp_sum(s0[rr]);
-          const T b = warp_sum(s1[rr]);
-          if (lane == 0) {
-            red_s[warp][2 * rr] = (double)a;
-            red_s[warp][2 * rr + 1] = (double)b;
-          }
+      for (int rr = 0; rr < TR; ++rr) {
+        const T a = warp_sum(s0[rr]);
+        const T b = warp_sum(s1[rr]);
+        if (lane == 0) {
+          red_s[t & 1][warp][2 * rr] = (double)a;
+          red_s[t & 1][warp][2 * rr + 1] = (double)b;
         }
       }
     }
-    __syncthreads();  // A
-    if (is_epi) {
-      if (lane < g) {   // ---- epilogue of group t ----
-        const int rr = lane;
-        double dots[2] = {0.0, 0.0};
-        for (int w = 0; w < kFusedWarps; ++w) {
-          dots[0] += red_s[w][2 * rr];
-          dots[1] += red_s[w][2 * rr + 1];
-        }
-        double w0, w1;
-        epi.finish(r0 + j0 + rr, in_next, dots, ered, eflags, w0, w1);
-        w_s[t & 1][rr][0] = (T)w0;
-        w_s[t & 1][rr][1] = (T)w1;
-      }
-      const int64_t jn = j0 + tr + lane;   // prefetch the inputs of group t+1
-      if (lane < tr && jn < nrows) in_next = epi.load_in(r0 + jn);
-    } else if (t >= 1) {
-      // ---- C(t-1): column pass of the previous group ----
-      const int64_t jp = j0 - tr;
-      const int gp = (int)min((int64_t)tr, nrows - jp);
+    if (t >= 2) {        // ---- C(t-2) ----
+      const int64_t j0 = (t - 2) * TR;
+      const int g = (int)min((int64_t)TR, nrows - j0);
 #pragma unroll
-      for (int rr = 0; rr < kMaxTR; ++rr) {
-        if (rr < gp) {
-          const int slot = (int)((jp + rr) % nslot);
+      for (int rr = 0; rr < TR; ++rr) {
+        if (rr < g) {
+          const int slot = (int)((j0 + rr) % nslot);
           const V* row = reinterpret_cast<const V*>(smem_raw + (size_t)slot * row_bytes);
-          const T w0 = w_s[(t - 1) & 1][rr][0], w1 = w_s[(t - 1) & 1][rr][1];
+          const T w0 = w_s[t & 1][rr][0], w1 = w_s[t & 1][rr][1];
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
             const int64_t c = tid + (int64_t)v * kFusedThreads;
@@ -279,12 +288,12 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
         }
       }
     }
-    __syncthreads();  // B
-    if (tid == 0 && t >= 1) {   // refill the slots of group t-1
-      const int64_t jp = j0 - tr;
-      const int gp = (int)min((int64_t)tr, nrows - jp);
-      for (int rr = 0; rr < gp; ++rr) {
-        const int64_t jn = jp + rr + nslot;
+    __syncthreads();
+    if (tid == 0 && t >= 2) {   // refill the slots of group t-2
+      const int64_t j0 = (t - 2) * TR;
+      const int g = (int)min((int64_t)TR, nrows - j0);
+      for (int rr = 0; rr < g; ++rr) {
+        const int64_t jn = j0 + rr + nslot;
         if (jn < nrows) {
           const int slot = (int)(jn % nslot);
           mbar_arrive_expect_tx(&full[slot], (unsigned)row_bytes);
@@ -293,27 +302,18 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
       }
     }
   }
-  if (!is_epi) {   // column partials of this CTA (one slab)
+  // column partials of this CTA (one slab)
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const int64_t c = tid + (int64_t)v * kFusedThreads;
-      if (c < nvec) {
-        double* p0 = cpart + ((int64_t)blockIdx.x * 2) * ld + c * VN;
-        double* p1 = cpart + ((int64_t)blockIdx.x * 2 + 1) * ld + c * VN;
+  for (int v = 0; v < NV; ++v) {
+    const int64_t c = tid + (int64_t)v * kFusedThreads;
+    if (c < nvec) {
+      double* p0 = cpart + ((int64_t)blockIdx.x * 2) * ld + c * VN;
+      double* p1 = cpart + ((int64_t)blockIdx.x * 2 + 1) * ld + c * VN;
 #pragma unroll
-        for (int i = 0; i < VN; ++i) {
-          p0[i] = (double)vget(ca[v], i);
-          p1[i] = (double)vget(cb[v], i);
-        }
+      for (int i = 0; i < VN; ++i) {
+        p0[i] = (double)vget(ca[v], i);
+        p1[i] = (double)vget(cb[v], i);
       }
-    }
-  } else {         // epilogue partials, held by the epilogue warp
-#pragma unroll
-    for (int k = 0; k < NR; ++k) ered[k] = warp_sum(ered[k]);
-    eflags = warp_or(eflags);
-    if (lane == 0) {
-      for (int k = 0; k < NR; ++k) rpart[blockIdx.x * (NR + 1) + k] = ered[k];
-      rpart[blockIdx.x * (NR + 1) + NR] = (double)eflags;
     }
   }
 }

@@ -64,7 +64,15 @@ struct YEpi {
   int64_t m;
   double alpha;
   int warm_x;
+  // controller scalars, cached in registers by begin() (fused kernel)
+  int64_t k_ = -1;
+  double rho_ = 0.0, ratio_ = 1.0;
   __device__ bool active() const { return ctl->status == GF_STATUS_RUNNING; }
+  __device__ void begin() {
+    k_ = ctl->k;
+    rho_ = ctl->rho;
+    ratio_ = ctl->ratio;
+  }
   __device__ void row(int64_t i, const double* dots, double* red, unsigned& flags) const {
     double w0, w1;
     row_w(i, dots, red, flags, w0, w1);
@@ -90,15 +98,16 @@ struct YEpi {
   }
   __device__ void finish(int64_t i, const RowIn& in, const double* dots, double* red, unsigned& flags,
                          double& w0, double& w1) const {
-    const int64_t k = ctl->k;
-    const double rho = ctl->rho;
+    const bool cached = k_ >= 0;
+    const int64_t k = cached ? k_ : ctl->k;
+    const double rho = cached ? rho_ : ctl->rho;
     double ykv, ytv;
     if (k == 0) {
       ykv = warm_x ? dots[0] : in.yk;
       ytv = in.yt;
     } else {
       ykv = dots[0];                          // y+ = A_hat x+  (projection.py:122)
-      ytv = M_(S_(in.cy, ykv), ctl->ratio);   // y~ + r_y - y+, rescaled (solver.py:420, :237)
+      ytv = M_(S_(in.cy, ykv), cached ? ratio_ : ctl->ratio);   // y~ + r_y - y+, rescaled (solver.py:420, :237)
     }
     if (!isfinite(ykv)) flags |= kBadYPlus;
     const double di = in.di;
@@ -468,44 +477,46 @@ static YEpi<T> make_yepi(gf_solver* s) {
   return y;
 }
 
-template <typename T, int NV>
-static void fused_attr(size_t smem) {
-  GF_CUDA(cudaFuncSetAttribute(fused_rowcol_kernel<T, NV, YEpi<T>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
-}
-
-template <typename T>
-static void fused_prepare(gf_solver* s) {
-  switch (s->fplan.nv) {
-    case 1: fused_attr<T, 1>(s->fplan.smem); break;
-    case 2: fused_attr<T, 2>(s->fplan.smem); break;
-    case 3: fused_attr<T, 3>(s->fplan.smem); break;
-    case 4: fused_attr<T, 4>(s->fplan.smem); break;
-    case 5: fused_attr<T, 5>(s->fplan.smem); break;
-    default: fused_attr<T, 6>(s->fplan.smem); break;
-  }
-}
-
-template <typename T, int NV>
-static void fused_launch_nv(gf_solver* s, cudaStream_t st) {
+// attr_only: set the dynamic shared-memory limit of the instance (at create)
+template <typename T, int NV, int TR>
+static void fused_go(gf_solver* s, cudaStream_t st, bool attr_only) {
   const FusedPlan& p = s->fplan;
-  fused_rowcol_kernel<T, NV, YEpi<T>><<<p.grid, kFusedCTA, p.smem, st>>>(
-      (const T*)s->S->A->data, s->m, s->ld, s->xk_T.as<T>(), s->xh_T.as<T>(), make_yepi<T>(s), p.nslot, p.tr,
-      s->rpart.as<double>(), s->cpart.as<double>());
+  auto kern = fused_rowcol_kernel<T, NV, TR, YEpi<T>>;
+  if (attr_only) {
+    GF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    return;
+  }
+  kern<<<p.grid, kFusedCTA, p.smem, st>>>((const T*)s->S->A->data, s->m, s->ld, s->xk_T.as<T>(), s->xh_T.as<T>(),
+                                          make_yepi<T>(s), p.nslot, s->rpart.as<double>(), s->cpart.as<double>());
   GF_CHECK_LAUNCH();
 }
 
-template <typename T>
-static void launch_fused(gf_solver* s, cudaStream_t st) {
-  switch (s->fplan.nv) {
-    case 1: fused_launch_nv<T, 1>(s, st); break;
-    case 2: fused_launch_nv<T, 2>(s, st); break;
-    case 3: fused_launch_nv<T, 3>(s, st); break;
-    case 4: fused_launch_nv<T, 4>(s, st); break;
-    case 5: fused_launch_nv<T, 5>(s, st); break;
-    default: fused_launch_nv<T, 6>(s, st); break;
+template <typename T, int NV>
+static void fused_tr(gf_solver* s, cudaStream_t st, bool attr_only) {
+  switch (s->fplan.tr) {
+    case 4: fused_go<T, NV, 4>(s, st, attr_only); break;
+    case 2: fused_go<T, NV, 2>(s, st, attr_only); break;
+    default: fused_go<T, NV, 1>(s, st, attr_only); break;
   }
 }
+
+template <typename T>
+static void fused_dispatch(gf_solver* s, cudaStream_t st, bool attr_only) {
+  switch (s->fplan.nv) {
+    case 1: fused_tr<T, 1>(s, st, attr_only); break;
+    case 2: fused_tr<T, 2>(s, st, attr_only); break;
+    case 3: fused_tr<T, 3>(s, st, attr_only); break;
+    case 4: fused_tr<T, 4>(s, st, attr_only); break;
+    case 5: fused_tr<T, 5>(s, st, attr_only); break;
+    default: fused_tr<T, 6>(s, st, attr_only); break;
+  }
+}
+
+template <typename T>
+static void fused_prepare(gf_solver* s) { fused_dispatch<T>(s, nullptr, true); }
+
+template <typename T>
+static void launch_fused(gf_solver* s, cudaStream_t st) { fused_dispatch<T>(s, st, false); }
 
 template <typename T>
 static XEpi<T> make_xepi(gf_solver* s) {
