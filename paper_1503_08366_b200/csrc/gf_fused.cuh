@@ -219,42 +219,49 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
     return;
   }
   // ===================== compute warps =====================
+  // 32-bit, incremental ring bookkeeping: the row pass walks (slotR, phaseR),
+  // the column pass slotC, and the refill walks slotF -- no div/mod per row.
   V xa[NV], xb[NV], ca[NV], cb[NV];
+  bool valid[NV];
   {
     const V* xv0 = reinterpret_cast<const V*>(x0);
     const V* xv1 = reinterpret_cast<const V*>(x1);
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      const int64_t c = tid + (int64_t)v * kFusedThreads;
-      xa[v] = c < nvec ? xv0[c] : V{};
-      xb[v] = c < nvec ? xv1[c] : V{};
+      const int c = tid + v * kFusedThreads;
+      valid[v] = c < (int)nvec;
+      xa[v] = valid[v] ? xv0[c] : V{};
+      xb[v] = valid[v] ? xv1[c] : V{};
       ca[v] = V{};
       cb[v] = V{};
     }
   }
-  for (int64_t t = 0; t < ngroups + 2; ++t) {
-    if (t < ngroups) {   // ---- R(t) ----
-      const int64_t j0 = t * TR;
-      const int g = (int)min((int64_t)TR, nrows - j0);
+  const unsigned rb = (unsigned)row_bytes;
+  const int nr = (int)nrows;
+  int slotR = 0, slotC = 0, slotF = 0;
+  unsigned phaseR = 0;
+  int jR = 0, jC = 0, jF = nslot;   // next row index for R / C / refill
+  const int ng = (int)ngroups;
+  for (int t = 0; t < ng + 2; ++t) {
+    if (t < ng) {   // ---- R(t) ----
       T s0[TR], s1[TR];
 #pragma unroll
       for (int rr = 0; rr < TR; ++rr) {
         s0[rr] = 0;
         s1[rr] = 0;
-        if (rr < g) {
-          const int64_t j = j0 + rr;
-          const int slot = (int)(j % nslot);
-          mbar_wait(&full[slot], (unsigned)((j / nslot) & 1));
-          const V* row = reinterpret_cast<const V*>(smem_raw + (size_t)slot * row_bytes);
+        if (jR < nr) {
+          mbar_wait(&full[slotR], phaseR);
+          const V* row = reinterpret_cast<const V*>(smem_raw + slotR * rb);
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
-            const int64_t c = tid + (int64_t)v * kFusedThreads;
-            if (c < nvec) {
-              const V a = row[c];
+            if (valid[v]) {
+              const V a = row[tid + v * kFusedThreads];
               s0[rr] = vdot(a, xa[v], s0[rr]);
               s1[rr] = vdot(a, xb[v], s1[rr]);
             }
           }
+          ++jR;
+          if (++slotR == nslot) { slotR = 0; phaseR ^= 1u; }
         }
       }
 #pragma unroll
@@ -267,38 +274,36 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
         }
       }
     }
-    if (t >= 2) {        // ---- C(t-2) ----
-      const int64_t j0 = (t - 2) * TR;
-      const int g = (int)min((int64_t)TR, nrows - j0);
+    int gC = 0;
+    if (t >= 2) {   // ---- C(t-2) ----
 #pragma unroll
       for (int rr = 0; rr < TR; ++rr) {
-        if (rr < g) {
-          const int slot = (int)((j0 + rr) % nslot);
-          const V* row = reinterpret_cast<const V*>(smem_raw + (size_t)slot * row_bytes);
+        if (jC < nr) {
+          const V* row = reinterpret_cast<const V*>(smem_raw + slotC * rb);
           const T w0 = w_s[t & 1][rr][0], w1 = w_s[t & 1][rr][1];
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
-            const int64_t c = tid + (int64_t)v * kFusedThreads;
-            if (c < nvec) {
-              const V a = row[c];
+            if (valid[v]) {
+              const V a = row[tid + v * kFusedThreads];
               vaxpy(ca[v], a, w0);
               vaxpy(cb[v], a, w1);
             }
           }
+          ++jC;
+          ++gC;
+          if (++slotC == nslot) slotC = 0;
         }
       }
     }
     __syncthreads();
-    if (tid == 0 && t >= 2) {   // refill the slots of group t-2
-      const int64_t j0 = (t - 2) * TR;
-      const int g = (int)min((int64_t)TR, nrows - j0);
-      for (int rr = 0; rr < g; ++rr) {
-        const int64_t jn = j0 + rr + nslot;
-        if (jn < nrows) {
-          const int slot = (int)(jn % nslot);
-          mbar_arrive_expect_tx(&full[slot], (unsigned)row_bytes);
-          bulk_g2s(smem_raw + (size_t)slot * row_bytes, A + (r0 + jn) * ld, (unsigned)row_bytes, &full[slot], pol);
+    if (tid == 0) {   // refill the slots the column pass just released
+      for (int rr = 0; rr < gC; ++rr) {
+        if (jF < nr) {
+          mbar_arrive_expect_tx(&full[slotF], rb);
+          bulk_g2s(smem_raw + slotF * rb, A + (r0 + jF) * ld, rb, &full[slotF], pol);
         }
+        ++jF;
+        if (++slotF == nslot) slotF = 0;
       }
     }
   }
@@ -306,7 +311,7 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     const int64_t c = tid + (int64_t)v * kFusedThreads;
-    if (c < nvec) {
+    if (valid[v]) {
       double* p0 = cpart + ((int64_t)blockIdx.x * 2) * ld + c * VN;
       double* p1 = cpart + ((int64_t)blockIdx.x * 2 + 1) * ld + c * VN;
 #pragma unroll
