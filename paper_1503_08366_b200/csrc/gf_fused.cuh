@@ -135,45 +135,107 @@ inline FusedPlan plan_fused(int64_t m, int64_t ld, int esize, int sms, size_t sm
   return p;
 }
 
+// All-lane sum of K values per lane in 5 + (K-1) shuffles instead of 5K: the
+// first log2(K) butterfly stages split the values between lane halves, so
+// after them lane l holds the partial of value (l >> (5 - log2 K))
+// ... of its half; the remaining stages are plain xor reductions.  Returns, in
+// lanes whose index selects value q, the full sum of value q; the caller reads
+// value q from lane q << (5 - log2 K).
+template <int K, typename T>
+__device__ __forceinline__ T warp_multi_sum(T (&v)[K], int lane) {
+  static_assert(K == 1 || K == 2 || K == 4 || K == 8, "K must be 1, 2, 4 or 8");
+  constexpr int LG = K == 1 ? 0 : (K == 2 ? 1 : (K == 4 ? 2 : 3));
+#pragma unroll
+  for (int s = 0; s < LG; ++s) {
+    const int off = 16 >> s;                 // 16, 8, 4
+    const bool upper = (lane & off) != 0;
+    constexpr int dummy = 0;
+    (void)dummy;
+    const int half = K >> (s + 1);           // values kept after this stage
+#pragma unroll
+    for (int q = 0; q < half; ++q) {
+      // lanes in the lower half keep value q, the upper half keeps value q + half
+      const T send = upper ? v[q] : v[q + half];
+      const T keep = upper ? v[q + half] : v[q];
+      v[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  T r = v[0];
+#pragma unroll
+  for (int off = 16 >> LG; off > 0; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
+  return r;
+}
+
 // Epi must provide: NR, active(), begin(), RowIn, load_in(i),
 // finish(i, in, dots, red, flags, w0, w1)   (YEpi in gf_solver.cu does).
+//
+// Warp roles (no CTA-wide barrier after setup; every hand-off is an mbarrier):
+//   warps 0..15  compute   R(t): dots of group t -> red_s[t&1] (arrive redf)
+//                          C(t-2): column pass with w_s[t&1]  (wait wf, arrive we;
+//                          arrive sfree[slot] per row consumed)
+//   warp 16      epilogue  wait redf -> reduce -> arrive rede; wait we ->
+//                          y-side epilogue -> w_s -> arrive wf
+//   warp 17      producer  wait sfree[slot] -> TMA bulk copy of the row NSLOT ahead
+constexpr int kEpiWarp = kFusedWarps;        // 16
+constexpr int kProdWarp = kFusedWarps + 1;   // 17
+constexpr int kFusedAll = kFusedThreads + 2 * kWarp;
+
 template <typename T, int NV, int TR, class Epi>
-__global__ void __launch_bounds__(kFusedCTA, 1)
+__global__ void __launch_bounds__(kFusedAll, 1)
 fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* __restrict__ x0,
                     const T* __restrict__ x1, Epi epi, int nslot, double* __restrict__ rpart,
                     double* __restrict__ cpart) {
   using V = typename Vec16<T>::type;
   constexpr int VN = Vec16<T>::n;
   constexpr int NR = Epi::NR;
+  constexpr int K = 2 * TR;
+  constexpr int LGK = K == 2 ? 1 : (K == 4 ? 2 : 3);
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[kMaxSlots];
-  __shared__ double red_s[2][kFusedWarps][2 * TR];
+  __shared__ __align__(8) uint64_t full[kMaxSlots], sfree[kMaxSlots];
+  __shared__ __align__(8) uint64_t redf[2], rede[2], wf[2], we[2];
+  __shared__ T red_s[2][kFusedWarps][K];
   __shared__ T w_s[2][TR][2];
 
   if (!epi.active()) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool is_epi = warp == kFusedWarps;
   const int64_t nvec = ld / VN;
-  const size_t row_bytes = (size_t)ld * sizeof(T);
+  const unsigned rb = (unsigned)(ld * sizeof(T));
   const int64_t r0 = rows * blockIdx.x / gridDim.x;   // contiguous, balanced row range
   const int64_t r1 = rows * (blockIdx.x + 1) / gridDim.x;
-  const int64_t nrows = r1 - r0;
-  const int64_t ngroups = (nrows + TR - 1) / TR;
+  const int nr = (int)(r1 - r0);
+  const int ng = (nr + TR - 1) / TR;
 
   if (tid == 0) {
-    for (int s = 0; s < nslot; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < nslot; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&sfree[s], kFusedWarps);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&redf[b], kFusedWarps);
+      mbar_init(&rede[b], 1);
+      mbar_init(&wf[b], 1);
+      mbar_init(&we[b], kFusedWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  uint64_t pol = 0;
-  if (tid == 0) {
-    pol = policy_evict_first();
-    for (int s = 0; s < nslot && s < nrows; ++s) {
-      mbar_arrive_expect_tx(&full[s], (unsigned)row_bytes);
-      bulk_g2s(smem_raw + (size_t)s * row_bytes, A + (r0 + s) * ld, (unsigned)row_bytes, &full[s], pol);
+
+  if (warp == kProdWarp) {
+    // ===================== producer warp =====================
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int slot = 0;
+      for (int j = 0; j < nr; ++j) {
+        if (j >= nslot) mbar_wait(&sfree[slot], (unsigned)(((j / nslot) - 1) & 1));
+        mbar_arrive_expect_tx(&full[slot], rb);
+        bulk_g2s(smem_raw + slot * rb, A + (r0 + j) * ld, rb, &full[slot], pol);
+        if (++slot == nslot) slot = 0;
+      }
     }
+    return;
   }
-  if (is_epi) {
+
+  if (warp == kEpiWarp) {
     // ===================== epilogue warp =====================
     epi.begin();
     double ered[NR > 0 ? NR : 1];
@@ -181,33 +243,37 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
     for (int k = 0; k < (NR > 0 ? NR : 1); ++k) ered[k] = 0.0;
     unsigned eflags = 0;
     typename Epi::RowIn in{};
-    if (lane < TR && lane < nrows) in = epi.load_in(r0 + lane);
-    for (int64_t t = 0; t < ngroups + 2; ++t) {
-      const int64_t ge = t - 1;   // group whose epilogue runs now
-      if (ge >= 0 && ge < ngroups) {
-        const int g = (int)min((int64_t)TR, nrows - ge * TR);
-        // cross-warp reduction of the 2*TR dots: lanes 0..15 hold one warp each
-        double v[2 * TR];
+    if (lane < TR && lane < nr) in = epi.load_in(r0 + lane);
+    for (int ge = 0; ge < ng; ++ge) {
+      const int b = ge & 1;
+      const unsigned use = (unsigned)(ge >> 1);
+      mbar_wait(&redf[b], use & 1u);
+      // fixed-order tree over the 16 compute warps: lanes 0..15 load one warp each
+      double v[K];
 #pragma unroll
-        for (int q = 0; q < 2 * TR; ++q) v[q] = lane < kFusedWarps ? red_s[ge & 1][lane][q] : 0.0;
+      for (int q = 0; q < K; ++q) v[q] = lane < kFusedWarps ? (double)red_s[b][lane][q] : 0.0;
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&rede[b], 0);   // red_s[b] may be rewritten
 #pragma unroll
-        for (int q = 0; q < 2 * TR; ++q)
+      for (int q = 0; q < K; ++q)
 #pragma unroll
-          for (int o = 8; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o, 16);
-        if (lane < g) {
-          double dots[2] = {0.0, 0.0};
+        for (int o = 8; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o, 16);
+      if (ge >= 2) mbar_wait(&we[b], (use - 1) & 1u);     // w_s[b] consumed by C(ge-2)
+      const int g = min(TR, nr - ge * TR);
+      if (lane < g) {
+        double dots[2] = {0.0, 0.0};
 #pragma unroll
-          for (int rr = 0; rr < TR; ++rr)
-            if (rr == lane) { dots[0] = v[2 * rr]; dots[1] = v[2 * rr + 1]; }
-          double w0, w1;
-          epi.finish(r0 + ge * TR + lane, in, dots, ered, eflags, w0, w1);
-          w_s[ge & 1][lane][0] = (T)w0;
-          w_s[ge & 1][lane][1] = (T)w1;
-        }
-        const int64_t jn = (ge + 1) * TR + lane;   // prefetch the inputs of the next group
-        if (lane < TR && jn < nrows) in = epi.load_in(r0 + jn);
+        for (int rr = 0; rr < TR; ++rr)
+          if (rr == lane) { dots[0] = v[2 * rr]; dots[1] = v[2 * rr + 1]; }
+        double w0, w1;
+        epi.finish(r0 + (int64_t)ge * TR + lane, in, dots, ered, eflags, w0, w1);
+        w_s[b][lane][0] = (T)w0;
+        w_s[b][lane][1] = (T)w1;
       }
-      __syncthreads();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&wf[b], 0);
+      const int jn = (ge + 1) * TR + lane;   // prefetch the inputs of the next group
+      if (lane < TR && jn < nr) in = epi.load_in(r0 + jn);
     }
 #pragma unroll
     for (int k = 0; k < NR; ++k) ered[k] = warp_sum(ered[k]);
@@ -218,9 +284,8 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
     }
     return;
   }
+
   // ===================== compute warps =====================
-  // 32-bit, incremental ring bookkeeping: the row pass walks (slotR, phaseR),
-  // the column pass slotC, and the refill walks slotF -- no div/mod per row.
   V xa[NV], xb[NV], ca[NV], cb[NV];
   bool valid[NV];
   {
@@ -236,19 +301,16 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
       cb[v] = V{};
     }
   }
-  const unsigned rb = (unsigned)row_bytes;
-  const int nr = (int)nrows;
-  int slotR = 0, slotC = 0, slotF = 0;
+  int slotR = 0, slotC = 0;
   unsigned phaseR = 0;
-  int jR = 0, jC = 0, jF = nslot;   // next row index for R / C / refill
-  const int ng = (int)ngroups;
+  int jR = 0, jC = 0;
   for (int t = 0; t < ng + 2; ++t) {
     if (t < ng) {   // ---- R(t) ----
-      T s0[TR], s1[TR];
+      T s[K];
 #pragma unroll
       for (int rr = 0; rr < TR; ++rr) {
-        s0[rr] = 0;
-        s1[rr] = 0;
+        s[2 * rr] = 0;
+        s[2 * rr + 1] = 0;
         if (jR < nr) {
           mbar_wait(&full[slotR], phaseR);
           const V* row = reinterpret_cast<const V*>(smem_raw + slotR * rb);
@@ -256,54 +318,48 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
           for (int v = 0; v < NV; ++v) {
             if (valid[v]) {
               const V a = row[tid + v * kFusedThreads];
-              s0[rr] = vdot(a, xa[v], s0[rr]);
-              s1[rr] = vdot(a, xb[v], s1[rr]);
+              s[2 * rr] = vdot(a, xa[v], s[2 * rr]);
+              s[2 * rr + 1] = vdot(a, xb[v], s[2 * rr + 1]);
             }
           }
           ++jR;
           if (++slotR == nslot) { slotR = 0; phaseR ^= 1u; }
         }
       }
-#pragma unroll
-      for (int rr = 0; rr < TR; ++rr) {
-        const T a = warp_sum(s0[rr]);
-        const T b = warp_sum(s1[rr]);
-        if (lane == 0) {
-          red_s[t & 1][warp][2 * rr] = (double)a;
-          red_s[t & 1][warp][2 * rr + 1] = (double)b;
-        }
-      }
+      const T tot = warp_multi_sum<K>(s, lane);   // lane (q << (5-LGK)) holds value q
+      const int b = t & 1;
+      const unsigned use = (unsigned)(t >> 1);
+      if (use >= 1) mbar_wait(&rede[b], (use - 1) & 1u);
+      if ((lane & ((32 >> LGK) - 1)) == 0) red_s[b][warp][lane >> (5 - LGK)] = tot;
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&redf[b], 0);
     }
-    int gC = 0;
     if (t >= 2) {   // ---- C(t-2) ----
+      const int b = t & 1;
+      const unsigned use = (unsigned)((t - 2) >> 1);
+      mbar_wait(&wf[b], use & 1u);
+      T w0[TR], w1[TR];
+#pragma unroll
+      for (int rr = 0; rr < TR; ++rr) { w0[rr] = w_s[b][rr][0]; w1[rr] = w_s[b][rr][1]; }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&we[b], 0);
 #pragma unroll
       for (int rr = 0; rr < TR; ++rr) {
         if (jC < nr) {
           const V* row = reinterpret_cast<const V*>(smem_raw + slotC * rb);
-          const T w0 = w_s[t & 1][rr][0], w1 = w_s[t & 1][rr][1];
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
             if (valid[v]) {
               const V a = row[tid + v * kFusedThreads];
-              vaxpy(ca[v], a, w0);
-              vaxpy(cb[v], a, w1);
+              vaxpy(ca[v], a, w0[rr]);
+              vaxpy(cb[v], a, w1[rr]);
             }
           }
+          __syncwarp();
+          if (lane == 0) mbar_arrive_expect_tx(&sfree[slotC], 0);
           ++jC;
-          ++gC;
           if (++slotC == nslot) slotC = 0;
         }
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {   // refill the slots the column pass just released
-      for (int rr = 0; rr < gC; ++rr) {
-        if (jF < nr) {
-          mbar_arrive_expect_tx(&full[slotF], rb);
-          bulk_g2s(smem_raw + slotF * rb, A + (r0 + jF) * ld, rb, &full[slotF], pol);
-        }
-        ++jF;
-        if (++slotF == nslot) slotF = 0;
       }
     }
   }

@@ -486,7 +486,7 @@ static void fused_go(gf_solver* s, cudaStream_t st, bool attr_only) {
     GF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
     return;
   }
-  kern<<<p.grid, kFusedCTA, p.smem, st>>>((const T*)s->S->A->data, s->m, s->ld, s->xk_T.as<T>(), s->xh_T.as<T>(),
+  kern<<<p.grid, kFusedAll, p.smem, st>>>((const T*)s->S->A->data, s->m, s->ld, s->xk_T.as<T>(), s->xh_T.as<T>(),
                                           make_yepi<T>(s), p.nslot, s->rpart.as<double>(), s->cpart.as<double>());
   GF_CHECK_LAUNCH();
 }
