@@ -173,12 +173,15 @@ __device__ __forceinline__ T warp_multi_sum(T (&v)[K], int lane) {
 //   warps 0..15  compute   R(t): dots of group t -> red_s[t&1] (arrive redf)
 //                          C(t-2): column pass with w_s[t&1]  (wait wf, arrive we;
 //                          arrive sfree[slot] per row consumed)
-//   warp 16      epilogue  wait redf -> reduce -> arrive rede; wait we ->
-//                          y-side epilogue -> w_s -> arrive wf
-//   warp 17      producer  wait sfree[slot] -> TMA bulk copy of the row NSLOT ahead
-constexpr int kEpiWarp = kFusedWarps;        // 16
-constexpr int kProdWarp = kFusedWarps + 1;   // 17
-constexpr int kFusedAll = kFusedThreads + 2 * kWarp;
+//   warps 16,17  epilogue  warp 16+b takes the groups of parity b (buffers b):
+//                          wait redf -> reduce -> arrive rede; wait we ->
+//                          y-side epilogue -> w_s -> arrive wf.  Two epilogue
+//                          warps double the rows in flight through the serial
+//                          fp64 epilogue, which is latency- not throughput-bound.
+//   warp 18      producer  wait sfree[slot] -> TMA bulk copy of the row NSLOT ahead
+constexpr int kEpiWarp = kFusedWarps;        // 16 and 17
+constexpr int kProdWarp = kFusedWarps + 2;   // 18
+constexpr int kFusedAll = kFusedThreads + 3 * kWarp;
 
 template <typename T, int NV, int TR, class Epi>
 __global__ void __launch_bounds__(kFusedAll, 1)
@@ -235,16 +238,17 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
     return;
   }
 
-  if (warp == kEpiWarp) {
-    // ===================== epilogue warp =====================
+  if (warp == kEpiWarp || warp == kEpiWarp + 1) {
+    // ===================== epilogue warps =====================
+    const int par = warp - kEpiWarp;
     epi.begin();
     double ered[NR > 0 ? NR : 1];
 #pragma unroll
     for (int k = 0; k < (NR > 0 ? NR : 1); ++k) ered[k] = 0.0;
     unsigned eflags = 0;
     typename Epi::RowIn in{};
-    if (lane < TR && lane < nr) in = epi.load_in(r0 + lane);
-    for (int ge = 0; ge < ng; ++ge) {
+    if (lane < TR && par * TR + lane < nr) in = epi.load_in(r0 + par * TR + lane);
+    for (int ge = par; ge < ng; ge += 2) {
       const int b = ge & 1;
       const unsigned use = (unsigned)(ge >> 1);
       mbar_wait(&redf[b], use & 1u);
@@ -272,15 +276,16 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(&wf[b], 0);
-      const int jn = (ge + 1) * TR + lane;   // prefetch the inputs of the next group
+      const int jn = (ge + 2) * TR + lane;   // prefetch the inputs of this warp's next group
       if (lane < TR && jn < nr) in = epi.load_in(r0 + jn);
     }
 #pragma unroll
     for (int k = 0; k < NR; ++k) ered[k] = warp_sum(ered[k]);
     eflags = warp_or(eflags);
-    if (lane == 0) {
-      for (int k = 0; k < NR; ++k) rpart[blockIdx.x * (NR + 1) + k] = ered[k];
-      rpart[blockIdx.x * (NR + 1) + NR] = (double)eflags;
+    if (lane == 0) {   // one partial record per epilogue warp: rpart[2 * cta + par]
+      double* out = rpart + (2 * (int64_t)blockIdx.x + par) * (NR + 1);
+      for (int k = 0; k < NR; ++k) out[k] = ered[k];
+      out[NR] = (double)eflags;
     }
     return;
   }

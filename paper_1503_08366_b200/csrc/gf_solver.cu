@@ -551,7 +551,7 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
       launch_fused<T>(s, st);
       s->mark(7, st, false);
       slabs = s->fplan.grid;
-      nrpart = s->fplan.grid;
+      nrpart = 2 * s->fplan.grid;   // one record per epilogue warp
       s->launches += 1;
     } else {             // two passes: row pass (+ y side), then column pass
       s->mark(1, st, true);
@@ -688,7 +688,7 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
     }
   }
   const int64_t nslab = std::max<int64_t>(s->cplan.slabs, s->fplan.ok ? s->fplan.grid : 1);
-  vec(s->rpart, std::max<int64_t>(s->grid_r, s->fplan.ok ? s->fplan.grid : 1) * (kRedY + 1));
+  vec(s->rpart, std::max<int64_t>(s->grid_r, s->fplan.ok ? 2 * s->fplan.grid : 1) * (kRedY + 1));
   vec(s->xpart, s->grid_s * (kRedX + 1));
   vec(s->zpart, s->grid_z);
   vec(s->red, 2 * s->ld + kScal);

@@ -124,11 +124,17 @@ __device__ __forceinline__ double prox_term(const Term& t, double rho, double v)
   const bool zc = t.c == 0.0;
   const int kind = zc ? kZero : t.h;
   const double ceff = zc ? 1.0 : t.c;
-  const double den = A_(t.e, rho);
-  const double rho_h = D_(den, M_(M_(ceff, t.a), t.a));
-  const double z0 = S_(D_(M_(t.a, S_(M_(v, rho), t.d)), den), t.b);
+  // x*1, x/1, x+0 (e = 0) and x-0 (d = 0) are exact in IEEE arithmetic, so
+  // skipping them for unit parameters changes no bit of the result but
+  // shortens the dependent fp64 chain (divisions dominate it).
+  const double den = t.e == 0.0 ? rho : A_(t.e, rho);
+  const double cas = M_(M_(ceff, t.a), t.a);
+  const double rho_h = cas == 1.0 ? den : D_(den, cas);
+  const double num = t.d == 0.0 ? M_(v, rho) : S_(M_(v, rho), t.d);
+  const double z0 = S_(D_(t.a == 1.0 ? num : M_(t.a, num), den), t.b);
   const double z = prox_base(kind, rho_h, z0);
-  return D_(A_(z, t.b), t.a);
+  const double zb = A_(z, t.b);
+  return t.a == 1.0 ? zb : D_(zb, t.a);
 }
 
 // h(x) with +inf off-domain (functions.py:77-105).
