@@ -11,23 +11,23 @@
 //
 // Structure: one persistent CTA per SM over a contiguous row range; a ring of
 // NSLOT row slots in shared memory filled by TMA bulk copies (cp.async.bulk,
-// L2 evict_first, one mbarrier per slot).  16 compute warps own fixed 16-byte
-// column vectors (x^ and x^_1/2 for them, and the column accumulators, live in
-// registers for the whole kernel); one epilogue warp runs the y side.  Rows
-// move in groups of TR through a three-stage software pipeline with ONE CTA
-// barrier per group:
+// L2 evict_first, one mbarrier per slot) issued by a producer warp.  16
+// compute warps own fixed 16-byte column vectors (x^ and x^_1/2 for them, and
+// the column accumulators, live in registers for the whole kernel); two
+// epilogue warps run the y side.  Rows move in groups of TR through a
+// three-stage software pipeline whose hand-offs are all mbarriers (no
+// CTA-wide barrier after setup):
 //
-//   iteration t:  compute warps   R(t)   dots of group t        -> red_s[t&1]
-//                                 C(t-2) A' [c_y, nu^] of group t-2 with w_s[t&1]
-//                 epilogue warp   E(t-1) reduce red_s[(t-1)&1]; y side of group
-//                                 t-1 (YEpi::finish) -> w_s[(t-1)&1]; prefetch
-//                                 the per-row inputs of group t
-//   --- barrier ---
-//                 thread 0        refill the slots of group t-2 (rows NSLOT ahead)
+//   compute warps   R(t)   dots of group t                    -> red_s[t&1]
+//                   C(t-2) A' [c_y, nu^] of group t-2 with w_s[t&1], then
+//                          release its slots to the producer
+//   epilogue warps  E(t)   (warp 16 + (t&1)) reduce red_s[t&1]; y side of
+//                          group t (YEpi::finish) -> w_s[t&1]
+//   producer warp          refill released slots with the rows NSLOT ahead
 //
 // so the serial per-row epilogue (fp64 prox, divisions, global stores) runs
-// concurrently with a row pass and a column pass instead of between them.
-// Three groups are resident; NSLOT - 3*TR rows are in flight from HBM.
+// concurrently with the row and column passes of other groups.  Three groups
+// are resident; NSLOT - 3*TR rows are in flight from HBM.
 #pragma once
 
 #include "gf_common.cuh"

@@ -34,6 +34,8 @@ namespace gf {
 struct Ctl {
   int status;
   unsigned ticket;
+  unsigned zflags;     // non-finite flags raised by the controller kernel's CTAs
+  unsigned pad_;
   int64_t k;           // iteration being assembled (R/C/Z) / prepared (S)
   int64_t iterations;  // SolveResult.iterations once terminated
   int64_t last_good;   // last recorded iteration, -1 if none
@@ -140,9 +142,10 @@ struct XEpi {
   TermsView g;
   const double* e;
   double *xk, *xt, *cx, *xh2, *muh2;
-  T *xk_T, *xh_T;
+  T *xk_T, *xh_T;   // row-pass right-hand sides: [x^ (tall) or c_x (wide), x^_1/2]
   int64_t n;
   double alpha;
+  int wide;          // wide orientation: the first right-hand side is c_x
   __device__ bool active() const { return ctl->status == GF_STATUS_RUNNING; }
   // init: x^, x~ given (warm start or zero) -- iteration 0 has no dual step.
   __device__ void apply(int64_t j, double xkv, double xtv, double* red, unsigned& flags) const {
@@ -161,7 +164,7 @@ struct XEpi {
     xh2[b + j] = xh;
     muh2[b + j] = mu;
     cx[j] = A_(rx, xtv);
-    xk_T[j] = (T)xkv;
+    xk_T[j] = (T)(wide ? A_(rx, xtv) : xkv);
     xh_T[j] = (T)xhh;
     const double mo = D_(mu, ej);
     red[0] += mo * mo;
@@ -174,6 +177,109 @@ struct XEpi {
     apply(j, xp, M_(S_(cx[j], xp), ctl->ratio), red, flags);            // solver.py:419, :237
   }
 };
+
+// ---------------------------------------------------------- wide (m < n) --
+// Row pass of the wide schedule: dots = [A_hat c_x, A_hat x^_1/2]; the y side
+// of iteration k (its y^ is the y+ of the previous projection, kept in ypl)
+// and the projection right-hand side A c - d (projection.py:124).
+template <typename T>
+struct YEpiW {
+  static constexpr int NR = kRedY;
+  Ctl* ctl;
+  TermsView f;
+  const double* d;
+  double *yk, *yt, *cy, *yh2, *nuh2;
+  const double* ypl;
+  T* rhs_T;
+  int64_t m;
+  double alpha;
+  __device__ bool active() const { return ctl->status == GF_STATUS_RUNNING; }
+  __device__ void row(int64_t i, const double* dots, double* red, unsigned& flags) const {
+    const int64_t k = ctl->k;
+    const double rho = ctl->rho;
+    double ykv, ytv;
+    if (k == 0) {
+      ykv = yk[i];
+      ytv = yt[i];
+    } else {
+      ykv = ypl[i];                                           // y+ of projection k-1
+      ytv = M_(S_(cy[i], ykv), ctl->ratio);                   // solver.py:420, :237
+    }
+    const double di = d[i];
+    const Term t = load_term(f, i);
+    const double yh = prox_term(t, M_(rho, M_(di, di)), D_(S_(ykv, ytv), di));
+    if (!isfinite(yh)) flags |= kBadYHalf;
+    const double yhh = M_(yh, di);
+    const double nu = M_(-rho, A_(S_(yhh, ykv), ytv));
+    const double ry = A_(M_(alpha, yhh), M_(S_(1.0, alpha), ykv));
+    const double cyn = A_(ry, ytv);
+    const int64_t b = (k & 1) * m;
+    yk[i] = ykv;
+    yt[i] = ytv;
+    yh2[b + i] = yh;
+    nuh2[b + i] = nu;
+    cy[i] = cyn;
+    rhs_T[i] = (T)S_(dots[0], cyn);                           // A c - d
+    const double rp = S_(D_(dots[1], di), yh);
+    red[0] += rp * rp;
+    red[1] += yh * yh;
+    red[2] += eval_term(t, yh);
+    red[3] += (yhh - ykv) * (yhh - ykv);
+  }
+};
+
+// Ginv pass of the wide schedule: w = (I + A A')^-1 (A c - d), y+ = d + w.
+struct WEpi {
+  static constexpr int NR = 0;
+  Ctl* ctl;
+  const double* cy;
+  double *w, *ypl;
+  __device__ bool active() const { return ctl->status == GF_STATUS_RUNNING; }
+  __device__ void row(int64_t i, const double* dots, double*, unsigned& flags) const {
+    w[i] = dots[0];
+    const double yp = A_(cy[i], dots[0]);                     // projection.py:125
+    ypl[i] = yp;
+    if (!isfinite(yp)) flags |= kBadYPlus;
+  }
+};
+
+// x side of the wide schedule after the controller: x+ = c_x - A_hat' w
+// (projection.py:126), dual step and prox_g of iteration k+1.
+template <typename T>
+__global__ void __launch_bounds__(256) x_wide_kernel(XEpi<T> epi, const double* __restrict__ aw,
+                                                     double* __restrict__ part) {
+  if (!epi.active()) return;
+  double red[kRedX] = {0.0, 0.0, 0.0};
+  unsigned flags = 0;
+  const double ratio = epi.ctl->ratio;
+  for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < epi.n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double cxj = epi.cx[j];
+    const double xp = S_(cxj, aw[j]);
+    epi.apply(j, xp, M_(S_(cxj, xp), ratio), red, flags);
+  }
+  __shared__ double sh[8][kRedX + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kRedX; ++k) red[k] = warp_sum(red[k]);
+  flags = warp_or(flags);
+  if (lane == 0) {
+    for (int k = 0; k < kRedX; ++k) sh[warp][k] = red[k];
+    sh[warp][kRedX] = (double)flags;
+  }
+  __syncthreads();
+  if (threadIdx.x <= kRedX) {
+    const int k = threadIdx.x;
+    if (k < kRedX) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += sh[w][k];
+      part[blockIdx.x * (kRedX + 1) + k] = s;
+    } else {
+      unsigned f = 0;
+      for (int w = 0; w < 8; ++w) f |= (unsigned)sh[w][kRedX];
+      part[blockIdx.x * (kRedX + 1) + kRedX] = (double)f;
+    }
+  }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(256) x_init_kernel(XEpi<T> epi, double* __restrict__ part) {
@@ -236,20 +342,29 @@ __global__ void y_scalars_kernel(const double* __restrict__ rpart, int64_t count
   }
 }
 
-// Z2: rhs and r_dual per column, then the controller in the last CTA.
-template <typename T>
+// Z2: per column the projection right-hand side (tall) or x+ (wide) and the
+// r_dual terms, then the controller in the last CTA.
+//   tall: red = [A_hat' c_y | A_hat' nu^ | y scalars]; rhs = c_x + A_hat' c_y
+//   wide: red = [A_hat' w   | A_hat' nu^ | y scalars]; x+ = c_x - A_hat' w
+//         (projection.py:124-126), y+ flags come from the Ginv pass (spart)
+template <typename T, bool WIDE>
 __global__ void __launch_bounds__(256)
 control_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ red, int64_t ld, int64_t n,
                const double* __restrict__ cx, const double* __restrict__ e, const double* __restrict__ muh2,
                T* __restrict__ rhs_T, double* __restrict__ zpart, const double* __restrict__ xpart,
-               int64_t nxpart, double* __restrict__ hist) {
+               int64_t nxpart, double* __restrict__ hist, const double* __restrict__ spart, int64_t nspart) {
   if (ctl->status != GF_STATUS_RUNNING) return;
   const int64_t k = ctl->k;
   const double* muh = muh2 + (k & 1) * n;
   double rd2 = 0.0;
+  unsigned zflag = 0;
   for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const double s1 = red[j], s2 = red[ld + j];
-    rhs_T[j] = (T)A_(cx[j], s1);                      // c + A_hat' d (projection.py:121)
+    if (WIDE) {
+      if (!isfinite(S_(cx[j], s1))) zflag |= kBadXPlus;
+    } else {
+      rhs_T[j] = (T)A_(cx[j], s1);                    // c + A_hat' d (projection.py:121)
+    }
     const double ej = e[j];
     const double rdj = A_(D_(s2, ej), D_(muh[j], ej)); // A' nu + mu in original space
     rd2 += rdj * rdj;
@@ -257,6 +372,8 @@ control_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ red
   __shared__ double sh[256];
   __shared__ bool last;
   sh[threadIdx.x] = rd2;
+  zflag = warp_or(zflag);
+  if ((threadIdx.x & 31) == 0 && zflag) atomicOr((unsigned*)&ctl->zflags, zflag);
   __syncthreads();
   for (int o = 128; o > 0; o >>= 1) {
     if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
@@ -297,12 +414,82 @@ control_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ red
     }
     __syncthreads();
   }
+  unsigned sflag = 0;   // wide: y+ = c_y + w flags of the Ginv pass
+  if (WIDE) {
+    unsigned f = 0;
+    for (int64_t i = threadIdx.x; i < nspart; i += blockDim.x) f |= (unsigned)spart[i];
+    sh[threadIdx.x] = (double)f;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int i = 0; i < 256; ++i) sflag |= (unsigned)sh[i];
+  }
   if (threadIdx.x != 0) return;
   double r2 = 0.0;
   for (unsigned b = 0; b < gridDim.x; ++b) r2 += zpart[b];
   ctl->ticket = 0;
+  const unsigned zf = ctl->zflags;
+  ctl->zflags = 0;
   const double* ys = red + 2 * ld;
   const unsigned xf = (unsigned)xs[kRedX];
+  if (WIDE) {
+    // order of solver.py: prox checks (:337), residual stop (:373), then the
+    // projection check (:414), then adapt_rho (:423)
+    const bool prox_bad = (xf & kBadXHalf) || ys[5] > 0.0;
+    const bool proj_bad = (zf & kBadXPlus) || (sflag & kBadYPlus);
+    if (prox_bad) {
+      ctl->status = GF_STATUS_DEGENERATE;
+      ctl->iterations = k;
+      ctl->final_rho = ctl->rho;
+      return;
+    }
+    const double rho = ctl->rho;
+    const double r_pri = sqrt(ys[0]);
+    const double r_dual = sqrt(r2);
+    const double eps_pri = prm.abs_tol + prm.rel_tol * sqrt(ys[1]);
+    const double eps_dual = prm.abs_tol + prm.rel_tol * sqrt(xs[0]);
+    const double obj = ys[2] + xs[1];
+    double* hrow = hist + k * 8;
+    hrow[0] = r_pri; hrow[1] = r_dual; hrow[2] = eps_pri; hrow[3] = eps_dual;
+    hrow[4] = rho; hrow[5] = obj; hrow[6] = sqrt(ys[3] + xs[2]); hrow[7] = (double)ctl->inner;
+    ctl->last_good = k;
+    ctl->r_pri = r_pri; ctl->r_dual = r_dual; ctl->eps_pri = eps_pri; ctl->eps_dual = eps_dual;
+    ctl->objective = obj;
+    if (r_pri <= eps_pri && r_dual <= eps_dual) {
+      ctl->status = GF_STATUS_SOLVED;
+      ctl->iterations = k + 1;
+      ctl->final_rho = rho;
+      return;
+    }
+    if (proj_bad) {
+      ctl->status = GF_STATUS_DEGENERATE;
+      ctl->iterations = k + 1;
+      ctl->final_rho = rho;
+      return;
+    }
+    double nrho = rho, ratio = 1.0;
+    if (prm.adaptive) {
+      if (r_dual < eps_dual && prm.tau * (double)k > (double)ctl->l_mark) {
+        nrho = prm.delta * rho;
+        ratio = rho / nrho;
+        ctl->u_mark = k;
+      } else if (r_pri < eps_pri && prm.tau * (double)k > (double)ctl->u_mark) {
+        nrho = rho / prm.delta;
+        ratio = rho / nrho;
+        ctl->l_mark = k;
+      }
+    }
+    ctl->rho_prev = rho;
+    ctl->rho = nrho;
+    ctl->ratio = ratio;
+    if (k + 1 >= prm.max_iter) {
+      ctl->status = GF_STATUS_MAX_ITERATIONS;
+      ctl->iterations = prm.max_iter;
+      ctl->final_rho = nrho;
+      return;
+    }
+    ctl->k = k + 1;
+    return;
+  }
   const bool proj_bad = (xf & kBadXPlus) || ys[4] > 0.0;
   const bool prox_bad = (xf & kBadXHalf) || ys[5] > 0.0;
   if (k >= prm.max_iter) {  // past the last iteration: only its projection check remains
@@ -410,6 +597,8 @@ struct gf_solver {
   gf_setup* S = nullptr;
   int dtype = GF_F64;
   int64_t m = 0, n = 0, ld = 0, q = 0, ldq = 0;
+  bool tall = true;
+  DBuf ypl, wv, spart;   // wide: y+ of the last projection, w, Ginv-pass flags
   Params prm{};
   TermsDev f, g;
   DBuf ctl, hist;
@@ -527,7 +716,7 @@ static XEpi<T> make_xepi(gf_solver* s) {
   x.xk = s->xk.as<double>(); x.xt = s->xt.as<double>(); x.cx = s->cx.as<double>();
   x.xh2 = s->xh2.as<double>(); x.muh2 = s->muh2.as<double>();
   x.xk_T = s->xk_T.as<T>(); x.xh_T = s->xh_T.as<T>();
-  x.n = s->n; x.alpha = s->prm.alpha;
+  x.n = s->n; x.alpha = s->prm.alpha; x.wide = s->tall ? 0 : 1;
   return x;
 }
 
@@ -588,12 +777,65 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
     s->mark(6, st, false);
   }
   s->mark(5, st, true);
-  control_kernel<T><<<(unsigned)s->grid_z, 256, 0, st>>>(
+  control_kernel<T, false><<<(unsigned)s->grid_z, 256, 0, st>>>(
       ctl, s->prm, s->red.as<double>(), s->ld, s->n, s->cx.as<double>(), s->S->e.as<double>(), s->muh2.as<double>(),
-      s->rhs_T.as<T>(), s->zpart.as<double>(), s->xpart.as<double>(), s->grid_s, s->hist.as<double>());
+      s->rhs_T.as<T>(), s->zpart.as<double>(), s->xpart.as<double>(), s->grid_s, s->hist.as<double>(), nullptr, 0);
   GF_CHECK_LAUNCH();
   s->mark(5, st, false);
   s->launches += 1;
+}
+
+// Wide step k (m < n): R(k) row pass [A c_x, A x^_1/2] + y side + rhs;
+// S(k) w = Ginv rhs, y+ = c_y + w; C(k) A' [w, nu^]; slab reduce; Z(k)
+// controller; X(k) x+ = c_x - A' w and the x side of iteration k+1.
+template <typename T>
+static void launch_step_wide(gf_solver* s, int64_t k, cudaStream_t st) {
+  gf_matrix* A = s->S->A;
+  gf_projector* P = s->S->P;
+  Ctl* ctl = s->ctl.as<Ctl>();
+  YEpiW<T> ye;
+  ye.ctl = ctl; ye.f = s->f.view; ye.d = s->S->d.as<double>();
+  ye.yk = s->yk.as<double>(); ye.yt = s->yt.as<double>(); ye.cy = s->cy.as<double>();
+  ye.yh2 = s->yh2.as<double>(); ye.nuh2 = s->nuh2.as<double>(); ye.ypl = s->ypl.as<double>();
+  ye.rhs_T = s->rhs_T.as<T>(); ye.m = s->m; ye.alpha = s->prm.alpha;
+  s->mark(1, st, true);
+  rowgemv_kernel<T, 2, YEpiW<T>><<<(unsigned)s->grid_r, kRowThreads, 0, st>>>(
+      (const T*)A->data, s->m, s->ld, s->xk_T.as<T>(), s->xh_T.as<T>(), ye, s->rpart.as<double>());
+  GF_CHECK_LAUNCH();
+  s->mark(1, st, false);
+  WEpi we{ctl, s->cy.as<double>(), s->wv.as<double>(), s->ypl.as<double>()};
+  s->mark(0, st, true);
+  rowgemv_kernel<T, 1, WEpi><<<(unsigned)s->grid_s, kRowThreads, 0, st>>>(
+      P->ginv.as<T>(), s->q, s->ldq, s->rhs_T.as<T>(), s->rhs_T.as<T>(), we, s->spart.as<double>());
+  GF_CHECK_LAUNCH();
+  s->mark(0, st, false);
+  s->mark(2, st, true);
+  colgemv_kernel<T, 2, false><<<dim3((unsigned)s->cplan.col_blocks, (unsigned)s->cplan.slabs), kColThreads, 0, st>>>(
+      (const T*)A->data, s->m, s->ld, s->wv.as<double>(), s->nuh2.as<double>() + (k & 1) * s->m,
+      s->cplan.rows_per_slab, s->cpart.as<double>(), &ctl->status);
+  GF_CHECK_LAUNCH();
+  s->mark(2, st, false);
+  s->mark(3, st, true);
+  colreduce_kernel<<<dim3((unsigned)ceil_div(s->ld, 32), 2), dim3(32, 8), 0, st>>>(
+      s->cpart.as<double>(), s->cplan.slabs, s->ld, 2, s->red.as<double>(), &ctl->status);
+  GF_CHECK_LAUNCH();
+  s->mark(3, st, false);
+  s->mark(4, st, true);
+  y_scalars_kernel<<<1, 256, 0, st>>>(s->rpart.as<double>(), s->grid_r, s->red.as<double>() + 2 * s->ld, ctl);
+  GF_CHECK_LAUNCH();
+  s->mark(4, st, false);
+  s->mark(5, st, true);
+  control_kernel<T, true><<<(unsigned)s->grid_z, 256, 0, st>>>(
+      ctl, s->prm, s->red.as<double>(), s->ld, s->n, s->cx.as<double>(), s->S->e.as<double>(), s->muh2.as<double>(),
+      s->rhs_T.as<T>(), s->zpart.as<double>(), s->xpart.as<double>(), s->grid_s, s->hist.as<double>(),
+      s->spart.as<double>(), s->grid_s);
+  GF_CHECK_LAUNCH();
+  s->mark(5, st, false);
+  s->mark(0, st, true);
+  x_wide_kernel<T><<<(unsigned)s->grid_s, 256, 0, st>>>(make_xepi<T>(s), s->red.as<double>(), s->xpart.as<double>());
+  GF_CHECK_LAUNCH();
+  s->mark(0, st, false);
+  s->launches += 7;
 }
 
 template <typename T>
@@ -618,6 +860,9 @@ static void solver_init(gf_solver* s, const double* x0, const double* nu0, doubl
     div_into<<<g, 256, 0, st>>>(tmp.as<double>(), n, rho0, s->xt.as<double>());
     GF_CHECK_LAUNCH();
   }
+  // wide warm start: y^ = A_hat x^0 (solver.py:302); the tall row pass of
+  // iteration 0 computes it on the fly instead (YEpi warm_x)
+  if (x0 && !s->tall && m > 0) matvec(s->S->A, false, s->xk.as<double>(), s->yk.as<double>(), st);
   x_init_kernel<T><<<(unsigned)s->grid_s, 256, 0, st>>>(make_xepi<T>(s), s->xpart.as<double>());
   GF_CHECK_LAUNCH();
   GF_CUDA(cudaStreamSynchronize(st));
@@ -652,9 +897,11 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
                          const double* x0, const double* nu0, cudaStream_t st) {
   GF_REQUIRE(S->P != nullptr, GF_E_PARAMETER, "setup has no projector");
   GF_REQUIRE(S->P->mode == 0, GF_E_UNSUPPORTED, "indirect projection is not available in this build");
-  GF_REQUIRE(S->P->tall, GF_E_UNSUPPORTED, "wide (m < n) problems are not available in this build");
+  GF_REQUIRE(S->P->tall || S->comm == nullptr || S->comm->nranks == 1, GF_E_UNSUPPORTED,
+             "wide (m < n) problems are solved on one GPU (row partitions need m >= n)");
   std::unique_ptr<gf_solver> s(new gf_solver());
   s->S = S;
+  s->tall = S->P->tall;
   gf_matrix* A = S->A;
   s->dtype = A->dtype;
   s->m = A->m; s->n = A->n; s->ld = A->ld; s->q = S->P->q; s->ldq = S->P->ldq;
@@ -681,7 +928,7 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
     GF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     s->fplan = plan_fused(s->m, s->ld, (int)es, sms, (size_t)optin);
     const char* env = getenv("GF_DISABLE_FUSED");
-    if (env && env[0] == '1') s->fplan.ok = false;
+    if ((env && env[0] == '1') || !s->tall) s->fplan.ok = false;
     if (s->fplan.ok) {
       if (s->dtype == GF_F32) fused_prepare<float>(s.get());
       else fused_prepare<double>(s.get());
@@ -692,6 +939,11 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
   vec(s->xpart, s->grid_s * (kRedX + 1));
   vec(s->zpart, s->grid_z);
   vec(s->red, 2 * s->ld + kScal);
+  if (!s->tall) {
+    vec(s->ypl, m1);
+    vec(s->wv, m1);
+    vec(s->spart, s->grid_s);
+  }
   s->cpart.alloc((size_t)nslab * 2 * s->ld * sizeof(double));
   const int64_t hrows = std::max<int64_t>(s->prm.max_iter, 1) + 1;
   vec(s->hist, hrows * 8);
@@ -728,8 +980,13 @@ void solver_run(gf_solver* s, int64_t steps, gf_solver_state* out, cudaStream_t 
     const int64_t nlaunch = std::min({chunk, budget, last_step - s->next_step + 1});
     GF_CUDA(cudaEventRecord(s->ev_a, st));
     for (int64_t i = 0; i < nlaunch; ++i) {
-      if (s->dtype == GF_F32) launch_step<float>(s, s->next_step, st);
-      else launch_step<double>(s, s->next_step, st);
+      if (s->tall) {
+        if (s->dtype == GF_F32) launch_step<float>(s, s->next_step, st);
+        else launch_step<double>(s, s->next_step, st);
+      } else if (s->next_step < s->prm.max_iter) {   // the wide controller ends at max_iter - 1
+        if (s->dtype == GF_F32) launch_step_wide<float>(s, s->next_step, st);
+        else launch_step_wide<double>(s, s->next_step, st);
+      }
       ++s->next_step;
     }
     GF_CUDA(cudaEventRecord(s->ev_b, st));
