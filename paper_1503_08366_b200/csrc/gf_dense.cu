@@ -131,6 +131,11 @@ void gram_accumulate(const gf_matrix* A, bool tall, double* G, int64_t ldg, cuda
   const int64_t q = tall ? A->n : A->m;
   if (A->dtype == GF_F32) {
     const float* a = (const float*)A->data;
+    const char* env = getenv("GF_GRAM_SIMT");
+    if (tall && !(env && env[0] == '1')) {   // tensor cores: tcgen05 3xTF32 (gf_syrk_tc.cu)
+      gram_tf32x3(A, G, ldg, st);
+      return;
+    }
     if (tall) gemm<float, float, true, false>(q, q, A->m, 1.0, a, A->ld, a, A->ld, 0.0, G, ldg, true, st);
     else gemm<float, float, false, true>(q, q, A->n, 1.0, a, A->ld, a, A->ld, 0.0, G, ldg, true, st);
   } else {

@@ -51,6 +51,7 @@ struct DBuf {
 
 // ------------------------------------------------ dense setup (gf_dense) --
 void gram_accumulate(const gf_matrix* A, bool tall, double* G, int64_t ldg, cudaStream_t st);
+void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st);  // tcgen05, G += A'A
 void gram_finish(double* G, int64_t q, int64_t ldg, cudaStream_t st);
 int cholesky(double* G, int64_t q, int64_t ld, int* d_info, cudaStream_t st);
 void trtri(double* L, int64_t q, int64_t ld, double* tmp, cudaStream_t st);

@@ -232,3 +232,18 @@ def test_c1_headline_values():
     res = gf.solve(_cases.build_problem(fx))
     assert res.status is gf.Status.SOLVED and res.iterations == 101
     assert res.objective == pytest.approx(252.42917798604532, rel=1e-9)
+
+
+@pytest.mark.parametrize("shape", [(513, 129), (3000, 700), (20000, 1300)])
+def test_gram_tensor_core_fp32(shape):
+    """The fp32 Gram runs on tcgen05 (3xTF32 split, fp64 drain every 4096
+    rows): it must agree with the fp64 Gram of the same fp32 data to
+    fp32-grade accuracy, including ragged tile edges."""
+    m, n = shape
+    A = np.random.default_rng(m + n).normal(size=(m, n)).astype(np.float32)
+    G = gf.build_projector(A).gram
+    A64 = A.astype(np.float64)
+    ref = A64.T @ A64 + np.eye(n)
+    err = np.abs(G - ref).max() / np.abs(ref).max()
+    assert err < 1e-6, err
+    np.testing.assert_allclose(G, G.T, rtol=0, atol=0)
