@@ -27,12 +27,15 @@
 namespace gf {
 namespace syrk {
 
+// K-major, no-swizzle operand layout (verified on B200 with tools/umma_probe.cu):
+// a core matrix is 8 MN-rows x 16 bytes (4 tf32 along K), 128 contiguous
+// bytes; 8-row groups are SBO = 128 B apart, 4-element K chunks LBO apart.
 constexpr int TM = 128, TN = 256, BK = 16, NST = 4;
 constexpr int KCHUNK = 4096;                       // rows per TMEM accumulation
-constexpr int A_BYTES = (BK / 8) * (TM / 4) * 128; // 8 KB per hi/lo
-constexpr int B_BYTES = (BK / 8) * (TN / 4) * 128; // 16 KB per hi/lo
-constexpr int LBO_A = (TM / 4) * 128;              // K-group stride
-constexpr int LBO_B = (TN / 4) * 128;
+constexpr int A_BYTES = (BK / 4) * (TM / 8) * 128; // 8 KB per hi/lo
+constexpr int B_BYTES = (BK / 4) * (TN / 8) * 128; // 16 KB per hi/lo
+constexpr int LBO_A = (TM / 8) * 128;              // K-chunk stride
+constexpr int LBO_B = (TN / 8) * 128;
 constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;   // 48 KB
 constexpr int SMEM = NST * STAGE;                  // 192 KB
 constexpr int NPROD = 8;                           // producer warps
@@ -65,7 +68,7 @@ __device__ __forceinline__ uint32_t to_tf32(float x) {
   return r;
 }
 
-// Shared-memory matrix descriptor: MN-major, no swizzle, Blackwell version 1.
+// Shared-memory matrix descriptor: no swizzle, Blackwell version 1.
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= (uint64_t)((addr & 0x3FFFF) >> 4);
@@ -75,8 +78,8 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
   return d;                 // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
 }
 
-// Instruction descriptor: D f32, A/B tf32, both MN-major, M = 128, N = 256.
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
+// Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 256.
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
                            ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
 
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
@@ -134,27 +137,31 @@ syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q
       if (it >= NST) bar_wait(&empty[s], (unsigned)(((it / NST) - 1) & 1));
       unsigned char* st = smem + (size_t)s * STAGE;
       const int64_t k0 = it * BK;
-#pragma unroll
-      for (int u = 0; u < (BK * (TM + TN) / 4) / (NPROD * 32); ++u) {
+      // item = (4-row K chunk kc, column c of the A|B panel): 4 coalesced
+      // 4-byte loads down the column, one 16-byte store of hi and one of lo
+      // (consecutive threads -> consecutive columns -> consecutive 16 B rows
+      // of a core matrix: conflict-free)
+#pragma unroll 2
+      for (int u = 0; u < ((BK / 4) * (TM + TN)) / (NPROD * 32); ++u) {
         const int idx = u * NPROD * 32 + pt;
-        const int r = idx / ((TM + TN) / 4);
-        const int c4 = idx % ((TM + TN) / 4);
-        const bool isA = c4 < TM / 4;
-        const int g = isA ? c4 : c4 - TM / 4;
-        const int64_t col = isA ? i0 + 4 * g : j0 + 4 * g;
-        const int64_t k = k0 + r;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (k < K && col < ld) v = __ldg(reinterpret_cast<const float4*>(A + k * ld + col));
+        const int kc = idx / (TM + TN);
+        const int c = idx % (TM + TN);
+        const bool isA = c < TM;
+        const int mn = isA ? c : c - TM;
+        const int64_t col = isA ? i0 + mn : j0 + mn;
+        const int64_t k = k0 + 4 * kc;
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = (k + e < K && col < ld) ? __ldg(A + (k + e) * ld + col) : 0.f;
         uint4 hi, lo;
-        hi.x = to_tf32(v.x); lo.x = to_tf32(v.x - __uint_as_float(hi.x));
-        hi.y = to_tf32(v.y); lo.y = to_tf32(v.y - __uint_as_float(hi.y));
-        hi.z = to_tf32(v.z); lo.z = to_tf32(v.z - __uint_as_float(hi.z));
-        hi.w = to_tf32(v.w); lo.w = to_tf32(v.w - __uint_as_float(hi.w));
-        const int kg = r >> 3, rr = r & 7;
+        hi.x = to_tf32(v[0]); lo.x = to_tf32(v[0] - __uint_as_float(hi.x));
+        hi.y = to_tf32(v[1]); lo.y = to_tf32(v[1] - __uint_as_float(hi.y));
+        hi.z = to_tf32(v[2]); lo.z = to_tf32(v[2] - __uint_as_float(hi.z));
+        hi.w = to_tf32(v[3]); lo.w = to_tf32(v[3] - __uint_as_float(hi.w));
         unsigned char* base_hi = isA ? st : st + 2 * A_BYTES;
         const int lbo = isA ? LBO_A : LBO_B;
         const int nb = isA ? A_BYTES : B_BYTES;
-        const int off = kg * lbo + g * 128 + rr * 16;
+        const int off = kc * lbo + (mn >> 3) * 128 + (mn & 7) * 16;
         *reinterpret_cast<uint4*>(base_hi + off) = hi;
         *reinterpret_cast<uint4*>(base_hi + nb + off) = lo;
       }
@@ -179,10 +186,11 @@ syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q
           const uint32_t a_hi = st, a_lo = st + A_BYTES, b_hi = st + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint64_t dah = smem_desc(a_hi + kk * LBO_A, LBO_A, 128);
-            const uint64_t dal = smem_desc(a_lo + kk * LBO_A, LBO_A, 128);
-            const uint64_t dbh = smem_desc(b_hi + kk * LBO_B, LBO_B, 128);
-            const uint64_t dbl = smem_desc(b_lo + kk * LBO_B, LBO_B, 128);
+            // one MMA covers K = 8 = two 4-element K chunks
+            const uint64_t dah = smem_desc(a_hi + 2 * kk * LBO_A, LBO_A, 128);
+            const uint64_t dal = smem_desc(a_lo + 2 * kk * LBO_A, LBO_A, 128);
+            const uint64_t dbh = smem_desc(b_hi + 2 * kk * LBO_B, LBO_B, 128);
+            const uint64_t dbl = smem_desc(b_lo + 2 * kk * LBO_B, LBO_B, 128);
             const uint32_t accum = (it > it0 || kk > 0) ? 1u : 0u;
             mma_tf32(d, dah, dbh, accum);
             mma_tf32(d, dah, dbl, 1u);
