@@ -8,16 +8,18 @@
 // hi = tf32(a), lo = tf32(a - hi) and
 //     G += hi_i' hi_j + hi_i' lo_j + lo_i' hi_j           (3 MMAs)
 // which keeps ~22 mantissa bits.  The accumulator lives in TMEM in fp32 and is
-// drained into the fp64 G every KCHUNK rows, so the long reduction over
-// m = 2e5 rows is carried in fp64.
+// drained into the fp64 G every `kchunk` rows: the tensor core's fp32
+// accumulation truncates, so its relative error grows with the number of
+// accumulate steps per drain (measured ~3e-8 per step); the drain interval
+// bounds it while the long reduction over m = 2e5 rows is carried in fp64.
 //
 // Tile: 128 columns of A (MMA M) x 256 columns (MMA N), lower-triangle tiles
 // only (G is mirrored afterwards).  Warp roles (416 threads):
 //   warps 0-3   epilogue: tcgen05.ld the 128x256 fp32 accumulator, add into G (fp64)
 //   warp 4      TMEM allocator + MMA issuer (one thread)
-//   warps 5-12  producers: LDG.128 of the fp32 rows, split into hi/lo, store
-//               to shared memory in the MN-major no-swizzle core-matrix layout
-//               the MMA descriptors expect (8 k-rows x 16 bytes per core matrix)
+//   warps 5-12  producers: coalesced column loads of 4 fp32 rows, split into
+//               hi/lo, one 16-byte store each into the K-major no-swizzle
+//               core-matrix layout the MMA descriptors expect
 // Pipelines: 4 shared-memory stages (full/empty mbarriers; empty is signalled
 // by tcgen05.commit) and 2 TMEM accumulators (256 columns each; full by
 // tcgen05.commit, empty by the epilogue warps).
@@ -31,7 +33,7 @@ namespace syrk {
 // a core matrix is 8 MN-rows x 16 bytes (4 tf32 along K), 128 contiguous
 // bytes; 8-row groups are SBO = 128 B apart, 4-element K chunks LBO apart.
 constexpr int TM = 128, TN = 256, BK = 16, NST = 4;
-constexpr int KCHUNK = 4096;                       // rows per TMEM accumulation
+constexpr int KCHUNK_DEFAULT = 1024;               // rows per TMEM accumulation (see gram_tf32x3)
 constexpr int A_BYTES = (BK / 4) * (TM / 8) * 128; // 8 KB per hi/lo
 constexpr int B_BYTES = (BK / 4) * (TN / 8) * 128; // 16 KB per hi/lo
 constexpr int LBO_A = (TM / 8) * 128;              // K-chunk stride
@@ -96,7 +98,7 @@ __device__ __forceinline__ void mma_commit(uint64_t* b) {
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
-syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q, const int2* __restrict__ tiles,
+syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q, int64_t kchunk, const int2* __restrict__ tiles,
                    double* __restrict__ G, int64_t ldg) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[NST], empty[NST], accf[2], acce[2];
@@ -105,8 +107,8 @@ syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q
   const int2 tile = tiles[blockIdx.x];
   const int64_t i0 = (int64_t)tile.x * TM, j0 = (int64_t)tile.y * TN;
   const int64_t nstages = (K + BK - 1) / BK;
-  const int64_t nchunks = (K + KCHUNK - 1) / KCHUNK;
-  constexpr int SPC = KCHUNK / BK;   // stages per chunk
+  const int64_t nchunks = (K + kchunk - 1) / kchunk;
+  const int64_t SPC = kchunk / BK;   // stages per chunk
 
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
@@ -260,7 +262,9 @@ void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st) {
     GF_CUDA(cudaFuncSetAttribute(syrk_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     attr = true;
   }
-  syrk_tf32x3_kernel<<<(unsigned)tl.size(), THREADS, SMEM, st>>>((const float*)A->data, A->m, A->ld, q,
+  const char* kc_env = getenv("GF_SYRK_KCHUNK");
+  int64_t kchunk = kc_env ? std::max<int64_t>(BK, atoll(kc_env) / BK * BK) : KCHUNK_DEFAULT;
+  syrk_tf32x3_kernel<<<(unsigned)tl.size(), THREADS, SMEM, st>>>((const float*)A->data, A->m, A->ld, q, kchunk,
                                                                  d_tiles.as<int2>(), G, ldg);
   GF_CHECK_LAUNCH();
   GF_CUDA(cudaStreamSynchronize(st));
