@@ -45,6 +45,39 @@ void allreduce_sum(gf_comm* c, double* buf, size_t count, cudaStream_t st) {
   if (r != ncclSuccess) throw_error(GF_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
 }
 
+// Setup phase timing (CUDA events), printed to stderr when GF_VERBOSE_SETUP=1.
+struct PhaseTimer {
+  cudaStream_t st;
+  bool on;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  explicit PhaseTimer(cudaStream_t s) : st(s) {
+    const char* e = getenv("GF_VERBOSE_SETUP");
+    on = e && e[0] == '1';
+    if (on) mark("start");
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    cudaEventRecord(ev, st);
+    marks.emplace_back(name, ev);
+  }
+  void report(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[gf] %s:", what);
+    for (size_t i = 1; i < marks.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
+      fprintf(stderr, " %s %.2f ms", marks[i].first.c_str(), ms);
+    }
+    fprintf(stderr, "\n");
+  }
+  ~PhaseTimer() {
+    for (auto& m : marks) cudaEventDestroy(m.second);
+  }
+};
+
 template <typename F>
 static int guarded(F&& fn) {
   try {
@@ -130,21 +163,27 @@ static gf_projector* projector_build(gf_matrix* A, int mode, double tol, int64_t
   const size_t gbytes = (size_t)std::max<int64_t>(q, 1) * P->ldg * sizeof(double);
   P->gram.alloc(gbytes);
   GF_CUDA(cudaMemsetAsync(P->gram.p, 0, gbytes, st));
+  PhaseTimer pt(st);
   if (A->m > 0 && A->n > 0) gram_accumulate(A, P->tall, P->gram.as<double>(), P->ldg, st);
   if (comm && comm->nranks > 1) allreduce_sum(comm, P->gram.as<double>(), (size_t)q * P->ldg, st);
   gram_finish(P->gram.as<double>(), q, P->ldg, st);
+  pt.mark("gram");
   DBuf L(gbytes), tmp(gbytes), inv(gbytes), info(sizeof(int));
   GF_CUDA(cudaMemcpyAsync(L.p, P->gram.p, gbytes, cudaMemcpyDeviceToDevice, st));
   const int bad = cholesky(L.as<double>(), q, P->ldg, info.as<int>(), st);
   if (bad != 0)
     throw_error(GF_E_NUMERIC, "Gram factorization failed: leading minor of order " + std::to_string(bad) +
                                   " is not positive definite");
+  pt.mark("cholesky");
   GF_CUDA(cudaMemsetAsync(tmp.p, 0, gbytes, st));
   trtri(L.as<double>(), q, P->ldg, tmp.as<double>(), st);
+  pt.mark("trtri");
   inverse_from_factor_inv(L.as<double>(), q, P->ldg, inv.as<double>(), st);
   P->ginv.alloc((size_t)std::max<int64_t>(q, 1) * P->ldq * A->esize());
   store_matrix(inv.as<double>(), P->ldg, A->dtype, P->ginv.p, P->ldq, q, q, st);
+  pt.mark("inverse");
   GF_CUDA(cudaStreamSynchronize(st));
+  pt.report("projector_build");
   return P.release();
 }
 
@@ -389,8 +428,12 @@ int gf_setup_create(gf_matrix* A, int equil, const double* d_in, const double* e
       copy_in(S->d.as<double>(), d_in, A->m, st);
       copy_in(S->e.as<double>(), e_in, A->n, st);
     } else if (equil) {
+      PhaseTimer pt(st);
       const EquilResult r = equilibrate(A, -1.0, -1.0, 300, comm, S->d.as<double>(), S->e.as<double>(), st);
+      pt.mark("equilibrate");
       rescale_even(A, S->d.as<double>(), S->e.as<double>(), comm, st);
+      pt.mark("rescale");
+      pt.report("setup");
       S->info.sweeps = r.sweeps;
       S->info.converged = r.converged ? 1 : 0;
       S->info.gamma = r.gamma;
