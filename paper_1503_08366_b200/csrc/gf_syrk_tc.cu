@@ -135,33 +135,45 @@ syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q
 
   if (warp >= 5) {
     // ===================== producers =====================
+    // item = (4-row K chunk kc, column c of the A|B panel): 4 coalesced 4-byte
+    // loads down the column, one 16-byte store of hi and one of lo
+    // (consecutive threads -> consecutive columns -> consecutive 16 B rows of
+    // a core matrix: conflict-free).  All loads of stage it+1 are in flight
+    // while stage it is converted (register double buffering).
+    constexpr int NITEM = ((BK / 4) * (TM + TN)) / (NPROD * 32);   // 6
     const int pt = tid - 5 * 32;   // 0..255
+    float cur[NITEM][4], nxt[NITEM][4];
+    auto load_stage = [&](int64_t it, float (&buf)[NITEM][4]) {
+      const int64_t k0 = it * BK;
+#pragma unroll
+      for (int u = 0; u < NITEM; ++u) {
+        const int idx = u * NPROD * 32 + pt;
+        const int kc = idx / (TM + TN);
+        const int c = idx % (TM + TN);
+        const int64_t col = c < TM ? i0 + c : j0 + (c - TM);
+        const int64_t k = k0 + 4 * kc;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) buf[u][e] = (k + e < K && col < ld) ? __ldg(A + (k + e) * ld + col) : 0.f;
+      }
+    };
+    load_stage(0, cur);
     for (int64_t it = 0; it < nstages; ++it) {
+      if (it + 1 < nstages) load_stage(it + 1, nxt);
       const int s = (int)(it % NST);
       if (it >= NST) bar_wait(&empty[s], (unsigned)(((it / NST) - 1) & 1));
       unsigned char* st = smem + (size_t)s * STAGE;
-      const int64_t k0 = it * BK;
-      // item = (4-row K chunk kc, column c of the A|B panel): 4 coalesced
-      // 4-byte loads down the column, one 16-byte store of hi and one of lo
-      // (consecutive threads -> consecutive columns -> consecutive 16 B rows
-      // of a core matrix: conflict-free)
-#pragma unroll 2
-      for (int u = 0; u < ((BK / 4) * (TM + TN)) / (NPROD * 32); ++u) {
+#pragma unroll
+      for (int u = 0; u < NITEM; ++u) {
         const int idx = u * NPROD * 32 + pt;
         const int kc = idx / (TM + TN);
         const int c = idx % (TM + TN);
         const bool isA = c < TM;
         const int mn = isA ? c : c - TM;
-        const int64_t col = isA ? i0 + mn : j0 + mn;
-        const int64_t k = k0 + 4 * kc;
-        float v[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) v[e] = (k + e < K && col < ld) ? __ldg(A + (k + e) * ld + col) : 0.f;
         uint4 hi, lo;
-        hi.x = to_tf32(v[0]); lo.x = to_tf32(v[0] - __uint_as_float(hi.x));
-        hi.y = to_tf32(v[1]); lo.y = to_tf32(v[1] - __uint_as_float(hi.y));
-        hi.z = to_tf32(v[2]); lo.z = to_tf32(v[2] - __uint_as_float(hi.z));
-        hi.w = to_tf32(v[3]); lo.w = to_tf32(v[3] - __uint_as_float(hi.w));
+        hi.x = to_tf32(cur[u][0]); lo.x = to_tf32(cur[u][0] - __uint_as_float(hi.x));
+        hi.y = to_tf32(cur[u][1]); lo.y = to_tf32(cur[u][1] - __uint_as_float(hi.y));
+        hi.z = to_tf32(cur[u][2]); lo.z = to_tf32(cur[u][2] - __uint_as_float(hi.z));
+        hi.w = to_tf32(cur[u][3]); lo.w = to_tf32(cur[u][3] - __uint_as_float(hi.w));
         unsigned char* base_hi = isA ? st : st + 2 * A_BYTES;
         const int lbo = isA ? LBO_A : LBO_B;
         const int nb = isA ? A_BYTES : B_BYTES;
@@ -172,6 +184,10 @@ syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) bar_arrive(&full[s]);
+#pragma unroll
+      for (int u = 0; u < NITEM; ++u)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cur[u][e] = nxt[u][e];
     }
   } else if (warp == 4) {
     // ===================== MMA issuer =====================
