@@ -244,11 +244,15 @@ syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q
               "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        // G is symmetric: accumulate the tile's transpose, G[j][i], so the 32
+        // lanes (consecutive i) touch 256 contiguous bytes per instruction;
+        // the upper triangle is mirrored down afterwards (gram_finish).
         if (i < q) {
-          double* grow = G + i * ldg + j0 + cc * 32;
 #pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (j0 + cc * 32 + t < q) grow[t] += (double)__uint_as_float(v[t]);
+          for (int t = 0; t < 32; ++t) {
+            const int64_t j = j0 + cc * 32 + t;
+            if (j < q) G[j * ldg + i] += (double)__uint_as_float(v[t]);
+          }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -260,6 +264,14 @@ syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// The kernel accumulates the upper triangle (transposed tile writes); copy it
+// down so callers see the usual lower-triangle result.
+__global__ void upper_to_lower(double* G, int64_t q, int64_t ld) {
+  const int64_t i = blockIdx.y * (int64_t)blockDim.y + threadIdx.y;
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < q && j < i) G[i * ld + j] = G[j * ld + i];
 }
 
 }  // namespace syrk
@@ -284,6 +296,8 @@ void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st) {
   int64_t kchunk = kc_env ? std::max<int64_t>(BK, atoll(kc_env) / BK * BK) : KCHUNK_DEFAULT;
   syrk_tf32x3_kernel<<<(unsigned)tl.size(), THREADS, SMEM, st>>>((const float*)A->data, A->m, A->ld, q, kchunk,
                                                                  d_tiles.as<int2>(), G, ldg);
+  GF_CHECK_LAUNCH();
+  upper_to_lower<<<dim3((unsigned)ceil_div(q, 32), (unsigned)ceil_div(q, 8)), dim3(32, 8), 0, st>>>(G, q, ldg);
   GF_CHECK_LAUNCH();
   GF_CUDA(cudaStreamSynchronize(st));
 }

@@ -245,5 +245,7 @@ def test_gram_tensor_core_fp32(shape):
     A64 = A.astype(np.float64)
     ref = A64.T @ A64 + np.eye(n)
     err = np.abs(G - ref).max() / np.abs(ref).max()
-    assert err < 1e-6, err
+    # the tensor core accumulates in truncating fp32 between fp64 drains every
+    # 512 rows: measured ~5e-6 (tools/syrk_accuracy.py); plain TF32 gives ~4e-4
+    assert err < 1.5e-5, err
     np.testing.assert_allclose(G, G.T, rtol=0, atol=0)
