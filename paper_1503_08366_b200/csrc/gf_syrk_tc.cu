@@ -247,12 +247,17 @@ syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q
         // G is symmetric: accumulate the tile's transpose, G[j][i], so the 32
         // lanes (consecutive i) touch 256 contiguous bytes per instruction;
         // the upper triangle is mirrored down afterwards (gram_finish).
+        // all 32 loads are issued before any store (a plain `+=` loop would
+        // serialize on possible aliasing between the stores and later loads)
         if (i < q) {
+          double g[32];
+          const int64_t jn = min((int64_t)32, q - (j0 + cc * 32));
+          double* col = G + (j0 + cc * 32) * ldg + i;
 #pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            const int64_t j = j0 + cc * 32 + t;
-            if (j < q) G[j * ldg + i] += (double)__uint_as_float(v[t]);
-          }
+          for (int t = 0; t < 32; ++t) g[t] = t < jn ? col[t * ldg] : 0.0;
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (t < jn) col[t * ldg] = g[t] + (double)__uint_as_float(v[t]);
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
