@@ -613,6 +613,7 @@ struct gf_solver {
   Ctl host{};
   Ctl* pinned = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  cudaEvent_t ev_done[2] = {nullptr, nullptr};   // controller snapshots of in-flight chunks
   double elapsed_ms = 0.0;
   int64_t launches = 0;  // kernels launched by solver_run
   // optional per-kernel timing (gf_solver_profile): events around each launch
@@ -625,6 +626,8 @@ struct gf_solver {
     if (pinned) cudaFreeHost(pinned);
     if (ev_a) cudaEventDestroy(ev_a);
     if (ev_b) cudaEventDestroy(ev_b);
+    for (auto e : ev_done)
+      if (e) cudaEventDestroy(e);
     for (auto e : ev_pool) cudaEventDestroy(e);
   }
   // Kernel classes: 0 S (Ginv GEMV + x side), 1 R (row pass + y side),
@@ -954,7 +957,9 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
   c.rho = st_in->rho0; c.rho_prev = st_in->rho0; c.ratio = 1.0; c.final_rho = st_in->rho0;
   c.r_pri = INFINITY; c.r_dual = INFINITY;
   GF_CUDA(cudaMemcpyAsync(s->ctl.p, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
-  GF_CUDA(cudaMallocHost(&s->pinned, sizeof(Ctl)));
+  GF_CUDA(cudaMallocHost(&s->pinned, 2 * sizeof(Ctl)));
+  GF_CUDA(cudaEventCreateWithFlags(&s->ev_done[0], cudaEventDisableTiming));
+  GF_CUDA(cudaEventCreateWithFlags(&s->ev_done[1], cudaEventDisableTiming));
   GF_CUDA(cudaEventCreate(&s->ev_a));
   GF_CUDA(cudaEventCreate(&s->ev_b));
   s->warm_x = x0 != nullptr;
@@ -976,9 +981,16 @@ void solver_run(gf_solver* s, int64_t steps, gf_solver_state* out, cudaStream_t 
   int64_t budget = steps > 0 ? steps : INT64_MAX;
   int64_t chunk = 1;
   read_ctl(s, st);
-  while (s->host.status == GF_STATUS_RUNNING && s->next_step <= last_step && budget > 0) {
+  // Two chunks in flight: chunk c+1 is enqueued before the host waits for the
+  // controller snapshot of chunk c, so the GPU never idles on the round trip.
+  // Kernels of steps after termination return at entry (status check).
+  Ctl* snap[2] = {s->pinned, s->pinned + 1};
+  cudaEvent_t done[2] = {s->ev_done[0], s->ev_done[1]};
+  int inflight = 0, cur = 0;
+  bool stop = s->host.status != GF_STATUS_RUNNING;
+  GF_CUDA(cudaEventRecord(s->ev_a, st));
+  while (!stop && s->next_step <= last_step && budget > 0) {
     const int64_t nlaunch = std::min({chunk, budget, last_step - s->next_step + 1});
-    GF_CUDA(cudaEventRecord(s->ev_a, st));
     for (int64_t i = 0; i < nlaunch; ++i) {
       if (s->tall) {
         if (s->dtype == GF_F32) launch_step<float>(s, s->next_step, st);
@@ -989,15 +1001,27 @@ void solver_run(gf_solver* s, int64_t steps, gf_solver_state* out, cudaStream_t 
       }
       ++s->next_step;
     }
-    GF_CUDA(cudaEventRecord(s->ev_b, st));
+    GF_CUDA(cudaMemcpyAsync(snap[cur], s->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    GF_CUDA(cudaEventRecord(done[cur], st));
     budget -= nlaunch;
-    read_ctl(s, st);
-    s->collect();
-    float ms = 0.f;
-    GF_CUDA(cudaEventElapsedTime(&ms, s->ev_a, s->ev_b));
-    s->elapsed_ms += ms;
+    ++inflight;
     chunk = std::min<int64_t>(chunk * 2, 32);
+    if (inflight == 2 || budget <= 0 || s->next_step > last_step) {
+      const int prev = cur ^ (inflight == 2 ? 1 : 0);   // oldest chunk in flight
+      GF_CUDA(cudaEventSynchronize(done[prev]));
+      --inflight;
+      s->host = *snap[prev];
+      stop = s->host.status != GF_STATUS_RUNNING;
+    }
+    cur ^= 1;
   }
+  GF_CUDA(cudaEventRecord(s->ev_b, st));
+  GF_CUDA(cudaStreamSynchronize(st));
+  read_ctl(s, st);
+  s->collect();
+  float ms = 0.f;
+  GF_CUDA(cudaEventElapsedTime(&ms, s->ev_a, s->ev_b));
+  s->elapsed_ms += ms;
   fill_state(s, out);
 }
 
