@@ -194,13 +194,30 @@ def run_ours(args):
     A_pin = torch.from_numpy(prob.A).pin_memory()
     prob_pin = gf.GraphFormProblem(A_pin, prob.f, prob.g)
     e2e_runs = []
-    for _ in range(2):   # first call warms module load / allocator
+    for _ in range(3):   # the first call warms module load / allocator; best of the rest
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = gf.solve(prob_pin)
         torch.cuda.synchronize()
         e2e_runs.append((time.perf_counter() - t0, res))
-    e2e_time, res = e2e_runs[-1]
+    e2e_time, res = min(e2e_runs[1:], key=lambda r: r[0]) if len(e2e_runs) > 1 else e2e_runs[-1]
+    # phase breakdown of the same public-API path (diagnostic, not the headline)
+    phases = {}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    setup_b = gf.prepare(prob_pin)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    run_b = slv._Run(setup_b, prob.f, prob.g, gf.SolverSettings(), None, None, m)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    run_b.run(0)
+    t3 = time.perf_counter()
+    run_b.result()
+    t4 = time.perf_counter()
+    phases = {"prepare_s": t1 - t0, "solver_create_s": t2 - t1, "iterate_s": t3 - t2, "result_s": t4 - t3,
+              "iterations": int(run_b.state.iterations)}
+    del run_b, setup_b
     h2d = prob.A.nbytes + sum(getattr(prob.f, k).nbytes for k in "abcde") + m \
         + sum(getattr(prob.g, k).nbytes for k in "abcde") + n
     d2h = 8 * (2 * m + 2 * n)
@@ -255,7 +272,8 @@ def run_ours(args):
                 "h2d_bytes_per_step": int(h2d / max(res.iterations, 1)),
                 "d2h_bytes_per_step": int(d2h / max(res.iterations, 1)),
                 "time_to_eps_s": e2e_time, "iterations": res.iterations, "status": res.status.value,
-                "objective": res.objective, "setup_s": res.setup_time, "h2d_bytes_total": int(h2d)},
+                "objective": res.objective, "setup_s": res.setup_time, "h2d_bytes_total": int(h2d),
+                "runs_s": [round(r[0], 4) for r in e2e_runs], "phases": phases},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "kernel": dom,
                      "algorithmic_bytes_per_launch": alg_bytes, "peak_kind": peaks_kind},

@@ -233,6 +233,10 @@ int gf_init(int device) {
     GF_CUDA(cudaSetDevice(device));
     GF_CUDA(cudaFree(0));
     num_sms();
+    cudaMemPool_t pool;
+    GF_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;   // retain freed blocks for reuse (DBuf)
+    GF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   });
 }
 
