@@ -410,10 +410,22 @@ int gf_project(gf_projector* P, const double* c, const double* d, double* x, dou
 int gf_project_indirect(gf_projector* P, const double* c, const double* d, const double* x_warm,
                         const double* y_warm, double tol, double* x, double* y, int64_t* iterations, int* converged,
                         void* stream) {
-  (void)P; (void)c; (void)d; (void)x_warm; (void)y_warm; (void)tol; (void)x; (void)y; (void)iterations;
-  (void)converged; (void)stream;
-  set_error("project_indirect (CGLS) is not available in this build");
-  return GF_E_UNSUPPORTED;
+  return guarded([&] {
+    GF_REQUIRE(tol > 0.0, GF_E_PARAMETER, "projection tolerance must be positive");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t m = P->A->m, n = P->A->n;
+    DevVec cv(c, n, st), dv(d, m, st), xw(x_warm, n, st), yw(y_warm, m, st);
+    DBuf xb(std::max<int64_t>(n, 1) * sizeof(double)), yb(std::max<int64_t>(m, 1) * sizeof(double));
+    bool ok = false;
+    const int64_t it = project_indirect_dev(P->A, P->tall, P->comm, cv.p, dv.p, x_warm ? xw.p : nullptr,
+                                            y_warm ? yw.p : nullptr, tol, P->max_inner, xb.as<double>(),
+                                            yb.as<double>(), &ok, st);
+    copy_out(x, xb.as<double>(), n, st);
+    copy_out(y, yb.as<double>(), m, st);
+    GF_CUDA(cudaStreamSynchronize(st));
+    if (iterations) *iterations = it;
+    if (converged) *converged = ok ? 1 : 0;
+  });
 }
 
 int gf_setup_create(gf_matrix* A, int equil, const double* d_in, const double* e_in, int mode, double tol,

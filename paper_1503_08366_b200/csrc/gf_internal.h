@@ -94,6 +94,13 @@ void prox_base(int kind, int64_t n, const double* rho, const double* v, double* 
 double evaluate(const TermsView& t, int64_t n, const double* v, cudaStream_t st);
 void eval_base(int kind, int64_t n, const double* x, double* out, cudaStream_t st);
 
+// ------------------------------------------------- CGLS indirect (gf_cgls) --
+int64_t cgls_solve(const gf_matrix* A, bool tall, gf_comm* comm, const double* h1, const double* h2, double* z,
+                   double tol, int64_t max_inner, bool* ok, cudaStream_t st);
+int64_t project_indirect_dev(const gf_matrix* A, bool tall, gf_comm* comm, const double* c, const double* d,
+                             const double* xw, const double* yw, double tol, int64_t max_inner, double* x,
+                             double* y, bool* ok, cudaStream_t st);
+
 // ------------------------------------------------------------- NCCL glue --
 void allreduce_sum(gf_comm* c, double* buf, size_t count, cudaStream_t st);
 

@@ -243,18 +243,21 @@ struct WEpi {
   }
 };
 
-// x side of the wide schedule after the controller: x+ = c_x - A_hat' w
-// (projection.py:126), dual step and prox_g of iteration k+1.
+// x side after the controller from an x+ given as a vector: wide schedule
+// x+ = c_x - A_hat' w (projection.py:126, sub = 1), or the CGLS solution of
+// the indirect mode (projection.py:148-150, sub = 0); then the dual step and
+// prox_g of iteration k+1.
 template <typename T>
 __global__ void __launch_bounds__(256) x_wide_kernel(XEpi<T> epi, const double* __restrict__ aw,
-                                                     double* __restrict__ part) {
+                                                     double* __restrict__ part, int sub) {
   if (!epi.active()) return;
   double red[kRedX] = {0.0, 0.0, 0.0};
   unsigned flags = 0;
   const double ratio = epi.ctl->ratio;
   for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < epi.n; j += (int64_t)gridDim.x * blockDim.x) {
     const double cxj = epi.cx[j];
-    const double xp = S_(cxj, aw[j]);
+    const double xp = sub ? S_(cxj, aw[j]) : aw[j];
+    if (!sub && !isfinite(xp)) flags |= kBadXPlus;
     epi.apply(j, xp, M_(S_(cxj, xp), ratio), red, flags);
   }
   __shared__ double sh[8][kRedX + 1];
@@ -598,7 +601,10 @@ struct gf_solver {
   int dtype = GF_F64;
   int64_t m = 0, n = 0, ld = 0, q = 0, ldq = 0;
   bool tall = true;
+  bool indirect = false;   // CGLS projection (projection.py:130-162)
+  double ptol = -1.0;      // fixed CGLS tolerance, <= 0: schedule
   DBuf ypl, wv, spart;   // wide: y+ of the last projection, w, Ginv-pass flags
+  DBuf xplus;            // indirect: CGLS iterate / x+
   Params prm{};
   TermsDev f, g;
   DBuf ctl, hist;
@@ -728,7 +734,29 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
   gf_matrix* A = s->S->A;
   gf_projector* P = s->S->P;
   Ctl* ctl = s->ctl.as<Ctl>();
-  if (k > 0) {  // S(k-1): x+ = Ginv rhs and the x side of iteration k
+  if (k > 0 && s->indirect) {
+    // Indirect projection of iteration k-1 (solver.py:397-411): CGLS on
+    // (I + A'A) x = c_x + A' c_y warm-started at x^, tolerance from the
+    // decreasing schedule min(1e-2, max(1e-10, 0.1 * drift)) unless fixed.
+    Ctl h;
+    GF_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    double drift = 0.0;
+    GF_CUDA(cudaMemcpyAsync(&drift, s->hist.as<double>() + (k - 1) * 8 + 6, sizeof(double), cudaMemcpyDeviceToHost,
+                            st));
+    GF_CUDA(cudaStreamSynchronize(st));
+    if (h.status != GF_STATUS_RUNNING) return;
+    const double ptol = s->ptol > 0.0 ? s->ptol : std::min(1e-2, std::max(1e-10, 0.1 * drift));
+    GF_CUDA(cudaMemcpyAsync(s->xplus.p, s->xk.p, s->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    bool ok = false;
+    const int64_t inner = cgls_solve(s->S->A, true, s->S->comm, s->cy.as<double>(), s->cx.as<double>(),
+                                     s->xplus.as<double>(), ptol, P->max_inner, &ok, st);
+    GF_CUDA(cudaMemcpyAsync(&ctl->inner, &inner, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    x_wide_kernel<T><<<(unsigned)s->grid_s, 256, 0, st>>>(make_xepi<T>(s), s->xplus.as<double>(),
+                                                            s->xpart.as<double>(), 0);
+    GF_CHECK_LAUNCH();
+    GF_CUDA(cudaStreamSynchronize(st));   // `inner` lives on this stack frame
+    s->launches += 1;
+  } else if (k > 0) {  // S(k-1): x+ = Ginv rhs and the x side of iteration k
     s->mark(0, st, true);
     rowgemv_kernel<T, 1, XEpi<T>><<<(unsigned)s->grid_s, kRowThreads, 0, st>>>(
         P->ginv.as<T>(), s->q, s->ldq, s->rhs_T.as<T>(), s->rhs_T.as<T>(), make_xepi<T>(s), s->xpart.as<double>());
@@ -835,7 +863,8 @@ static void launch_step_wide(gf_solver* s, int64_t k, cudaStream_t st) {
   GF_CHECK_LAUNCH();
   s->mark(5, st, false);
   s->mark(0, st, true);
-  x_wide_kernel<T><<<(unsigned)s->grid_s, 256, 0, st>>>(make_xepi<T>(s), s->red.as<double>(), s->xpart.as<double>());
+  x_wide_kernel<T><<<(unsigned)s->grid_s, 256, 0, st>>>(make_xepi<T>(s), s->red.as<double>(), s->xpart.as<double>(),
+                                                          1);
   GF_CHECK_LAUNCH();
   s->mark(0, st, false);
   s->launches += 7;
@@ -899,12 +928,15 @@ static void fill_state(gf_solver* s, gf_solver_state* st) {
 gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, const gf_settings* st_in,
                          const double* x0, const double* nu0, cudaStream_t st) {
   GF_REQUIRE(S->P != nullptr, GF_E_PARAMETER, "setup has no projector");
-  GF_REQUIRE(S->P->mode == 0, GF_E_UNSUPPORTED, "indirect projection is not available in this build");
+  GF_REQUIRE(S->P->mode == 0 || S->P->tall, GF_E_UNSUPPORTED,
+             "the indirect (CGLS) projection inside solve is available for tall problems (m >= n)");
   GF_REQUIRE(S->P->tall || S->comm == nullptr || S->comm->nranks == 1, GF_E_UNSUPPORTED,
              "wide (m < n) problems are solved on one GPU (row partitions need m >= n)");
   std::unique_ptr<gf_solver> s(new gf_solver());
   s->S = S;
   s->tall = S->P->tall;
+  s->indirect = S->P->mode == 1;
+  s->ptol = st_in->projection_tol;
   gf_matrix* A = S->A;
   s->dtype = A->dtype;
   s->m = A->m; s->n = A->n; s->ld = A->ld; s->q = S->P->q; s->ldq = S->P->ldq;
@@ -947,6 +979,7 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
     vec(s->wv, m1);
     vec(s->spart, s->grid_s);
   }
+  if (s->indirect) vec(s->xplus, n);
   s->cpart.alloc((size_t)nslab * 2 * s->ld * sizeof(double));
   const int64_t hrows = std::max<int64_t>(s->prm.max_iter, 1) + 1;
   vec(s->hist, hrows * 8);

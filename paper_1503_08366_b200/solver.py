@@ -301,6 +301,11 @@ def solve(problem: GraphFormProblem, settings: SolverSettings = None, *,
         seen = -1
         while True:
             st = run.run(1)
+            # a step begins with the (indirect) projection of the previous
+            # iteration: its CGLS count belongs to the previous snapshot
+            # (solver.py:410-411)
+            if trace and settings.projection == "indirect" and st.k > seen:
+                trace[-1].inner_iterations = int(st.inner_iterations)
             if st.k > seen:
                 k = int(st.k)
                 seen = k
@@ -315,8 +320,7 @@ def solve(problem: GraphFormProblem, settings: SolverSettings = None, *,
                     trace.append(IterationSnapshot(k=k, rho=float(rho), x_hat=xk, y_hat=yk, xt=xt, yt=yt,
                                                    x_half_hat=xhh, y_half_hat=yhh, r_pri=float(r_pri),
                                                    r_dual=float(r_dual), eps_pri=float(eps_pri),
-                                                   eps_dual=float(eps_dual),
-                                                   inner_iterations=int(st.inner_iterations)))
+                                                   eps_dual=float(eps_dual), inner_iterations=0))
             if st.status != 0:
                 break
     x, y, mu, nu, st = run.result()

@@ -110,6 +110,23 @@ def test_projection_matches_reference(name):
     np.testing.assert_allclose(x2, x, rtol=1e-9, atol=1e-10)
 
 
+@pytest.mark.parametrize("name", ["tall_70x25", "wide_25x70", "kkt_5x3"])
+def test_project_indirect_matches_reference(name):
+    """CGLS projection (projection.py:130-196) at tol 1e-10: same inner
+    iteration count and the same point as the reference."""
+    A, c, d = PR[f"{name}_A"], PR[f"{name}_c"], PR[f"{name}_d"]
+    P = gf.build_projector(A, mode="indirect", tol=1e-10)
+    r = gf.project_indirect(P, c, d)
+    assert r.iterations == int(PR[f"{name}_iiters"]) and r.converged
+    np.testing.assert_allclose(r.x, PR[f"{name}_ix"], rtol=1e-9, atol=1e-10)
+    np.testing.assert_allclose(r.y, PR[f"{name}_iy"], rtol=1e-9, atol=1e-10)
+    # warm start at the answer: (almost) no inner iterations (SPEC.md:269)
+    r2 = gf.project_indirect(P, c, d, x_warm=r.x, y_warm=r.y)
+    assert r2.iterations <= 1
+    with pytest.raises(gf.ParameterError):
+        gf.project(P, c, d)
+
+
 def test_projection_closed_forms():
     sig = np.array([0.5, 2.0, 3.0])
     P = gf.build_projector(np.diag(sig))               # SPEC.md:259-260
@@ -132,7 +149,7 @@ def test_projection_closed_forms():
 # reproduces the GPU value exactly).
 CHAOTIC = ("logistic_2000x200", "logistic_4000x400_prefix")
 SOLVE_FP64 = [n for n in _cases.solve_case_names()
-              if not n.endswith("_r32") and "indirect" not in n and n not in CHAOTIC]
+              if not n.endswith("_r32") and n not in CHAOTIC]
 
 
 @pytest.mark.parametrize("name", SOLVE_FP64)
