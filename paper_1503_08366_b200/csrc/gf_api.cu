@@ -40,7 +40,7 @@ int num_sms() {
 }
 
 void allreduce_sum(gf_comm* c, double* buf, size_t count, cudaStream_t st) {
-  if (c == nullptr || c->nranks <= 1 || count == 0) return;
+  if (!comm_active(c) || count == 0) return;
   const ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, st);
   if (r != ncclSuccess) throw_error(GF_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
 }
@@ -142,7 +142,7 @@ static gf_projector* projector_build(gf_matrix* A, int mode, double tol, int64_t
   P->mode = mode;
   P->comm = comm;
   P->tall = A->m >= A->n;   // projection.py:76 (global rows decide under a partition)
-  if (comm && comm->nranks > 1) {
+  if (comm_active(comm)) {
     DBuf b(sizeof(double));
     double mloc = (double)A->m;
     GF_CUDA(cudaMemcpyAsync(b.p, &mloc, sizeof(double), cudaMemcpyHostToDevice, st));
@@ -165,7 +165,7 @@ static gf_projector* projector_build(gf_matrix* A, int mode, double tol, int64_t
   GF_CUDA(cudaMemsetAsync(P->gram.p, 0, gbytes, st));
   PhaseTimer pt(st);
   if (A->m > 0 && A->n > 0) gram_accumulate(A, P->tall, P->gram.as<double>(), P->ldg, st);
-  if (comm && comm->nranks > 1) allreduce_sum(comm, P->gram.as<double>(), (size_t)q * P->ldg, st);
+  if (comm_active(comm)) allreduce_sum(comm, P->gram.as<double>(), (size_t)q * P->ldg, st);
   gram_finish(P->gram.as<double>(), q, P->ldg, st);
   pt.mark("gram");
   DBuf L(gbytes), tmp(gbytes), inv(gbytes), info(sizeof(int));
@@ -201,7 +201,7 @@ static void project_direct(gf_projector* P, const double* c, const double* d, do
     DBuf t(std::max<int64_t>(n, 1) * sizeof(double)), rhs(std::max<int64_t>(n, 1) * sizeof(double));
     GF_CUDA(cudaMemsetAsync(t.p, 0, t.bytes, st));
     if (m > 0) matvec(A, true, d, t.as<double>(), st);                 // A' d
-    if (P->comm && P->comm->nranks > 1) allreduce_sum(P->comm, t.as<double>(), n, st);
+    if (comm_active(P->comm)) allreduce_sum(P->comm, t.as<double>(), n, st);
     combine(c, 1.0, t.as<double>(), 1.0, rhs.as<double>(), n, st);     // c + A' d
     ginv_apply(P, rhs.as<double>(), x, st);                            // x = G^-1 (c + A' d)
     if (m > 0) matvec(A, false, x, y, st);                             // y = A x
@@ -555,7 +555,7 @@ int gf_comm_create(const char* id128, int nranks, int rank, gf_comm** out) {
     std::unique_ptr<gf_comm> c(new gf_comm());
     c->nranks = nranks;
     c->rank = rank;
-    if (nranks > 1) {
+    {   // a communicator even for one rank, so every collective call site is exercisable on one GPU
       ncclUniqueId id;
       std::memcpy(id.internal, id128, sizeof(id.internal));
       const ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);

@@ -67,7 +67,7 @@ struct Cgls {
   void rmv(const double* r, double* out) {
     if (nr() > 0) matvec(A, tall, r, out, st);
     else GF_CUDA(cudaMemsetAsync(out, 0, nz() * sizeof(double), st));
-    if (tall && comm && comm->nranks > 1) allreduce_sum(comm, out, nz(), st);
+    if (tall && comm_active(comm)) allreduce_sum(comm, out, nz(), st);
   }
   // dot of two vectors; `local` marks row-sharded (r-space) vectors
   double dot(const double* a, const double* b, int64_t n, bool local) {
@@ -80,7 +80,7 @@ struct Cgls {
       GF_CUDA(cudaMemsetAsync(scal.p, 0, sizeof(double), st));
     }
     GF_CHECK_LAUNCH();
-    if (local && comm && comm->nranks > 1) allreduce_sum(comm, scal.as<double>(), 1, st);
+    if (local && comm_active(comm)) allreduce_sum(comm, scal.as<double>(), 1, st);
     GF_CUDA(cudaMemcpyAsync(&v, scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     GF_CUDA(cudaStreamSynchronize(st));
     return v;

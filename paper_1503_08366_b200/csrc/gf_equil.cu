@@ -133,7 +133,7 @@ __global__ void square_into(const double* x, double* y, int64_t n) {
 static unsigned vgrid(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 1024)); }
 
 static double global_rows(gf_matrix* A, gf_comm* comm, cudaStream_t st) {
-  if (comm == nullptr || comm->nranks == 1) return (double)A->m;
+  if (!comm_active(comm)) return (double)A->m;
   DBuf b(sizeof(double));
   double m = (double)A->m;
   GF_CUDA(cudaMemcpyAsync(b.p, &m, sizeof(double), cudaMemcpyHostToDevice, st));
@@ -181,7 +181,7 @@ static EquilResult equil_t(gf_matrix* A, double gamma, double eps, int64_t max_i
       GF_CUDA(cudaMemsetAsync(scal.p, 0, 3 * sizeof(double), st));
       GF_CUDA(cudaMemsetAsync(csum.p, 0, ld * sizeof(double), st));
     }
-    if (comm && comm->nranks > 1) {
+    if (comm_active(comm)) {
       // [c (ld) | ddiff, rowsum, bad] reduced together
       GF_CUDA(cudaMemcpyAsync(csum.as<double>() + ld, scal.p, 3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
       allreduce_sum(comm, csum.as<double>(), ld + 3, st);
@@ -241,7 +241,7 @@ static void rescale_t(gf_matrix* A, double* d, double* e, gf_comm* comm, cudaStr
     GF_CHECK_LAUNCH();
     sum_parts<<<1, 256, 0, st>>>(rpart.as<double>(), rgrid, 3, scal.as<double>());
   }
-  if (comm && comm->nranks > 1) allreduce_sum(comm, scal.as<double>(), 3, st);
+  if (comm_active(comm)) allreduce_sum(comm, scal.as<double>(), 3, st);
   double h[3];
   GF_CUDA(cudaMemcpyAsync(h, scal.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
   GF_CUDA(cudaStreamSynchronize(st));

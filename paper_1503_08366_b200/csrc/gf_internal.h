@@ -27,6 +27,9 @@ struct gf_comm {
   int nranks = 1, rank = 0;
 };
 
+// true when collectives must run (a communicator exists, even of one rank)
+inline bool comm_active(const gf_comm* c) { return c != nullptr && c->comm != nullptr; }
+
 namespace gf {
 
 // Device buffer with RAII free, from the device's stream-ordered memory pool

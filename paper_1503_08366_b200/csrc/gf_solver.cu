@@ -802,7 +802,7 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
   } else {
     GF_CUDA(cudaMemsetAsync(s->red.p, 0, (2 * s->ld + kScal) * sizeof(double), st));
   }
-  if (s->S->comm && s->S->comm->nranks > 1) {
+  if (comm_active(s->S->comm)) {
     s->mark(6, st, true);
     allreduce_sum(s->S->comm, s->red.as<double>(), 2 * s->ld + kScal, st);
     s->mark(6, st, false);
@@ -888,7 +888,7 @@ static void solver_init(gf_solver* s, const double* x0, const double* nu0, doubl
     DBuf tmp(s->ld * sizeof(double));
     GF_CUDA(cudaMemsetAsync(tmp.p, 0, s->ld * sizeof(double), st));
     if (m > 0) matvec(s->S->A, true, nuhat0.as<double>(), tmp.as<double>(), st);
-    if (s->S->comm && s->S->comm->nranks > 1) allreduce_sum(s->S->comm, tmp.as<double>(), n, st);
+    if (comm_active(s->S->comm)) allreduce_sum(s->S->comm, tmp.as<double>(), n, st);
     div_into<<<g, 256, 0, st>>>(tmp.as<double>(), n, rho0, s->xt.as<double>());
     GF_CHECK_LAUNCH();
   }
@@ -930,7 +930,7 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
   GF_REQUIRE(S->P != nullptr, GF_E_PARAMETER, "setup has no projector");
   GF_REQUIRE(S->P->mode == 0 || S->P->tall, GF_E_UNSUPPORTED,
              "the indirect (CGLS) projection inside solve is available for tall problems (m >= n)");
-  GF_REQUIRE(S->P->tall || S->comm == nullptr || S->comm->nranks == 1, GF_E_UNSUPPORTED,
+  GF_REQUIRE(S->P->tall || !comm_active(S->comm), GF_E_UNSUPPORTED,
              "wide (m < n) problems are solved on one GPU (row partitions need m >= n)");
   std::unique_ptr<gf_solver> s(new gf_solver());
   s->S = S;

@@ -280,15 +280,18 @@ class _Run:
 def solve(problem: GraphFormProblem, settings: SolverSettings = None, *,
           x0=None, nu0=None, scaling: Optional[Equilibration] = None,
           setup: Optional[Setup] = None, callback: Optional[Callable] = None,
-          trace: Optional[list] = None) -> SolveResult:
-    """Solve minimize f(y) + g(x) s.t. y = A x (solver.py:248-437)."""
+          trace: Optional[list] = None, comm=None) -> SolveResult:
+    """Solve minimize f(y) + g(x) s.t. y = A x (solver.py:248-437).
+
+    ``comm`` (extension): a ``distributed.Comm`` when ``problem`` holds this
+    rank's rows of a row-partitioned problem (see ``distributed.py``)."""
     if settings is None:
         settings = SolverSettings()
     if settings.gap_stop:
         raise NotImplementedError("gap-based stopping is not in this build (SURVEY §8f)")
     own = setup is None
     if own:
-        setup = prepare(problem, settings, scaling=scaling)
+        setup = prepare(problem, settings, scaling=scaling, comm=comm)
     setup_time = setup.setup_time if own else 0.0
     t0 = time.perf_counter()
     run = _Run(setup, problem.f, problem.g, settings, x0, nu0, problem.m)
