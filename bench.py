@@ -181,34 +181,61 @@ def run_reference(args):
 def run_ours(args):
     import torch
     import paper_1503_08366_b200 as gf
-    from paper_1503_08366_b200 import _native, solver as slv
+    from paper_1503_08366_b200 import _native, distributed, solver as slv
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
-    if world > 1:
-        raise SystemExit("multi-GPU bench is not wired in this build yet")
-    m, n = args.m, args.n
-    prob, meta = build_instance(m, n)
     dev = torch.device("cuda", local)
+    comm = None
+    use_comm = world > 1 or args.force_comm
+    if use_comm:
+        import torch.distributed as dist
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        dist.init_process_group("nccl", device_id=dev)
+        comm = distributed.init_comm()
+
+    def sync():
+        torch.cuda.synchronize()
+        if use_comm:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        if use_comm:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    m, n = args.m, args.n
+    r0, r1 = distributed.row_range(m, rank, world)
+    full, meta = build_instance(m, n)
+    # this rank's rows (row partition); the host copy of the
+    # full matrix is dropped before any device work
+    prob = gf.GraphFormProblem(np.ascontiguousarray(full.A[r0:r1]), full.f.slice(r0, r1), full.g)
+    del full
+    m_loc = r1 - r0
     peaks, peaks_kind = measured_peaks()
     # ---------------- e2e: full solve from pinned host memory ----------------
     A_pin = torch.from_numpy(prob.A).pin_memory()
     prob_pin = gf.GraphFormProblem(A_pin, prob.f, prob.g)
     e2e_runs = []
     for _ in range(3):   # the first call warms module load / allocator; best of the rest
-        torch.cuda.synchronize()
+        sync()
         t0 = time.perf_counter()
-        res = gf.solve(prob_pin)
+        res = gf.solve(prob_pin, comm=comm)
         torch.cuda.synchronize()
-        e2e_runs.append((time.perf_counter() - t0, res))
+        e2e_runs.append((max_over_ranks([time.perf_counter() - t0])[0], res))
     e2e_time, res = min(e2e_runs[1:], key=lambda r: r[0]) if len(e2e_runs) > 1 else e2e_runs[-1]
     # phase breakdown of the same public-API path (diagnostic, not the headline)
-    phases = {}
-    torch.cuda.synchronize()
+    sync()
     t0 = time.perf_counter()
-    setup_b = gf.prepare(prob_pin)
+    setup_b = gf.prepare(prob_pin, comm=comm)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    run_b = slv._Run(setup_b, prob.f, prob.g, gf.SolverSettings(), None, None, m)
+    run_b = slv._Run(setup_b, prob.f, prob.g, gf.SolverSettings(), None, None, m_loc)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     run_b.run(0)
@@ -218,13 +245,13 @@ def run_ours(args):
     phases = {"prepare_s": t1 - t0, "solver_create_s": t2 - t1, "iterate_s": t3 - t2, "result_s": t4 - t3,
               "iterations": int(run_b.state.iterations)}
     del run_b, setup_b
-    h2d = prob.A.nbytes + sum(getattr(prob.f, k).nbytes for k in "abcde") + m \
+    h2d = prob.A.nbytes + sum(getattr(prob.f, k).nbytes for k in "abcde") + m_loc \
         + sum(getattr(prob.g, k).nbytes for k in "abcde") + n
-    d2h = 8 * (2 * m + 2 * n)
+    d2h = 8 * (2 * m_loc + 2 * n)
     # ---------------- device-resident iteration timing ----------------
-    setup = gf.prepare(prob)
+    setup = gf.prepare(prob, comm=comm)
     tight = gf.SolverSettings(abs_tol=1e-12, rel_tol=1e-12, max_iter=args.warmup + 2 * args.steps + 8)
-    run = slv._Run(setup, prob.f, prob.g, tight, None, None, m)
+    run = slv._Run(setup, prob.f, prob.g, tight, None, None, m_loc)
     run.run(args.warmup)
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -233,12 +260,12 @@ def run_ours(args):
     l0 = C.c_int64()
     _native.check(L.gf_solver_stats(run.handle, C.byref(l0), None, None))
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
+        sync()
         e0.record(stream)
         st = run.run(args.steps)
         e1.record(stream)
-        torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+        sync()
+    ms = max_over_ranks([e0.elapsed_time(e1)])[0]
     l1 = C.c_int64()
     _native.check(L.gf_solver_stats(run.handle, C.byref(l1), None, None))
     assert st.status == 0 and st.k + 1 == args.warmup + args.steps, (st.status, st.k)
@@ -253,11 +280,12 @@ def run_ours(args):
              "allreduce", "fused_rowcol_yside"]
     kernels = {names[i]: {"avg_ms": kms[i] / kcnt[i], "count": int(kcnt[i])} for i in range(8) if kcnt[i]}
     es = 4 if setup.dtype == _native.GF_F32 else 8
-    # dominant kernel: the pass over A_hat (fused single pass, or the row pass
-    # of the two-pass fallback); algorithmic bytes = m*n*s per launch
+    # dominant kernel: the pass over this rank's rows of A_hat (fused single
+    # pass, or the row pass of the two-pass fallback); algorithmic bytes =
+    # m_loc*n*s per launch
     dom = "fused_rowcol_yside" if "fused_rowcol_yside" in kernels else "row_pass_yside"
-    alg_bytes = m * n * es
-    t_row = kernels[dom]["avg_ms"] / 1e3
+    alg_bytes = m_loc * n * es
+    t_row = max_over_ranks([kernels[dom]["avg_ms"]])[0] / 1e3
     achieved = alg_bytes / t_row / 1e9
     peak = peaks["hbm_gbs"]
     line = {
@@ -266,7 +294,8 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32" if es == 4 else "f64",
         "data": "synthetic (reference Lasso recipe, seed 0, A rounded to fp32)",
         "config": {"workload": f"dense Lasso {m}x{n} fp32 (BASELINE configs[4], 1e9 coefficients)",
-                   "m": m, "n": n, "parallelism": f"row partition x{world}",
+                   "m": m, "n": n, "parallelism": f"row partition x{world}" + (" (NCCL all-reduce)" if use_comm else ""),
+                   "rows_per_rank": m_loc,
                    "l2": "A is 4 GB >> 126 MB L2; no flush needed"},
         "e2e": {"value": res.iterations / e2e_time, "unit": "iters/s",
                 "h2d_bytes_per_step": int(h2d / max(res.iterations, 1)),
@@ -281,10 +310,14 @@ def run_ours(args):
         "gpu_launches": int(l1.value - l0.value),
         "clocks": clk.summary(),
     }
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:
         line["cpu_baseline"] = cpu_baseline(prob, max(1, m // 10), iters=10)
     if rank == 0:
         print(json.dumps(line))
+    del run, setup
+    if use_comm:
+        del comm
+        dist.destroy_process_group()
     return 0
 
 
@@ -297,6 +330,8 @@ def main():
     ap.add_argument("--m", type=int, default=M_FULL)
     ap.add_argument("--n", type=int, default=N_FULL)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-comm", action="store_true",
+                    help="use the NCCL row-partition path even on one GPU (checks the multi-GPU plumbing)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

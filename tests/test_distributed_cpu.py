@@ -1,0 +1,177 @@
+"""CPU: the row-partitioned (multi-GPU) schedule, world size 2 over gloo.
+
+The device library runs a tall solve split by rows with one NCCL all-reduce
+per iteration.  These tests run the same
+decomposition on CPU -- ``oracle/sharded_oracle.py``, two processes, gloo --
+and require it to reproduce the reference goldens exactly as the
+single-process oracle does (iteration counts and statuses exactly, values to
+~1e-9), plus the host-side pieces of ``distributed.py`` (row ranges, the
+unique-id broadcast that builds the communicator).
+"""
+
+import ctypes
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import graphform_oracle as orc
+from oracle import sharded_oracle as sho
+from paper_1503_08366_b200 import distributed
+from tests import _cases
+
+CASES = ["lasso_tall_1000x200", "lasso_tall_1000x200_alpha", "lasso_tall_1000x200_fixedrho",
+         "lasso_tall_1000x200_indirect", "lasso_tall_1000x200_maxit", "lasso_tall_1000x200_noeq",
+         "huber_fit_400x80", "nnls_600x150", "svm_2000x100", "lp_600x240", "basis_pursuit_500x120"]
+# Not here: the logistic cases.  The reference's safeguarded Newton
+# (prox.py:27-48) exits unconverged after 100 steps for some coordinates
+# (e.g. rho_h = 0.031, z0 = 29: Newton oscillates across the root until the
+# bracket bisection takes over), so a 1-ulp change of its input -- which a
+# different row-summation order produces -- moves the prox by ~1e-4 and the
+# trajectory diverges from the golden one.  Those cases are compared on the
+# GPU with the scaling pinned (test_gpu_parity.py, CHAOTIC).
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _init(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _allreduce(a):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+    dist.all_reduce(t)
+    return t.numpy()
+
+
+def _solve_worker(rank, world, port, out_dir, names):
+    _init(rank, world, port)
+    try:
+        for name in names:
+            fx = _cases.load("solve_" + name)
+            prob = _cases.build_problem(fx)
+            A = np.asarray(prob.A, float)
+            m = A.shape[0]
+            r0, r1 = distributed.row_range(m, rank, world)
+            f = orc.Terms.of(prob.f)
+            f_loc = orc.Terms(*(getattr(f, k)[r0:r1] for k in "habcde"))
+            res = sho.solve(A[r0:r1], f_loc, orc.Terms.of(prob.g), m, _allreduce, _cases.settings_of(fx))
+            np.savez(os.path.join(out_dir, f"{name}_r{rank}.npz"), x=res["x"], y=res["y"], mu=res["mu"],
+                     nu=res["nu"], d=res["d"], e=res["e"], iterations=res["iterations"],
+                     status=res["status"], history=res["history"], r0=r0, r1=r1)
+    finally:
+        dist.destroy_process_group()
+
+
+def _close(a, b, rtol, atol=1e-12):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return np.linalg.norm(a - b) <= rtol * np.linalg.norm(b) + atol * np.sqrt(max(b.size, 1))
+
+
+@pytest.fixture(scope="module")
+def sharded_results(tmp_path_factory):
+    out = tmp_path_factory.mktemp("sharded")
+    mp.spawn(_solve_worker, args=(2, _free_port(), str(out), CASES), nprocs=2, join=True)
+    return out
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_row_partitioned_solve_matches_reference(sharded_results, name):
+    fx = _cases.load("solve_" + name)
+    parts = [dict(np.load(os.path.join(sharded_results, f"{name}_r{r}.npz"))) for r in range(2)]
+    for p in parts:
+        assert int(p["iterations"]) == int(fx["iterations"])
+        assert str(p["status"]) == str(fx["status"])
+        np.testing.assert_allclose(p["history"], fx["history"], rtol=1e-8, atol=1e-12)
+        # replicated side identical on every rank, equal to the reference
+        assert _close(p["x"], fx["x"], 1e-9) and _close(p["mu"], fx["mu"], 1e-9)
+    np.testing.assert_array_equal(parts[0]["x"], parts[1]["x"])
+    np.testing.assert_array_equal(parts[0]["e"], parts[1]["e"])
+    y = np.concatenate([p["y"] for p in parts])
+    nu = np.concatenate([p["nu"] for p in parts])
+    d = np.concatenate([p["d"] for p in parts])
+    assert _close(y, fx["y"], 1e-9) and _close(nu, fx["nu"], 1e-9)
+    if "noeq" not in name:
+        assert _close(d, fx["d"], 1e-10) and _close(parts[0]["e"], fx["e"], 1e-10)
+
+
+@pytest.mark.parametrize("m,world", [(10, 1), (10, 2), (7, 3), (200_000, 8), (5, 8)])
+def test_row_range_partitions_rows(m, world):
+    spans = [distributed.row_range(m, r, world) for r in range(world)]
+    assert spans[0][0] == 0 and spans[-1][1] == m
+    for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+        assert a1 == b0
+    sizes = [b - a for a, b in spans]
+    assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        distributed.row_range(m, world, world)
+
+
+class _FakeLib:
+    """Stands in for libgraphform on CPU: records the communicator calls."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.created = None
+
+    def gf_comm_unique_id(self, buf):
+        buf.raw = bytes(range(128))
+        return 0
+
+    def gf_comm_create(self, uid, nranks, rank, out):
+        self.created = (ctypes.string_at(uid, 128), nranks, rank)
+        return 0
+
+    def gf_comm_destroy(self, h):
+        return 0
+
+
+def _comm_worker(rank, world, port, out_dir):
+    _init(rank, world, port)
+    try:
+        fake = _FakeLib(rank)
+        distributed._native.lib = lambda: fake
+        distributed._native.check = lambda code: None
+        c = distributed.init_comm()
+        assert (c.rank, c.world) == (rank, world)
+        uid, n, r = fake.created
+        with open(os.path.join(out_dir, f"uid{rank}.bin"), "wb") as fh:
+            fh.write(bytes(uid))
+        assert (n, r) == (world, rank)
+        c.handle = None
+    finally:
+        dist.destroy_process_group()
+
+
+def test_init_comm_broadcasts_rank0_id(tmp_path):
+    mp.spawn(_comm_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    ids = [open(os.path.join(tmp_path, f"uid{r}.bin"), "rb").read() for r in range(2)]
+    # all 128 bytes (NUL bytes included) reach NCCL identically on every rank
+    assert ids[0] == ids[1] == bytes(range(128))
+
+
+def test_sharded_oracle_single_rank_is_the_oracle():
+    fx = _cases.load("solve_lasso_tall_1000x200")
+    prob = _cases.build_problem(fx)
+    A = np.asarray(prob.A, float)
+    a = sho.solve(A, orc.Terms.of(prob.f), orc.Terms.of(prob.g), A.shape[0], lambda v: np.array(v, float))
+    b = orc.solve(A, orc.Terms.of(prob.f), orc.Terms.of(prob.g))
+    assert a["iterations"] == b["iterations"]
+    np.testing.assert_allclose(a["history"], b["history"], rtol=1e-10, atol=1e-14)
+
+
+def test_sharded_oracle_rejects_wide():
+    A = np.ones((4, 8))
+    t = orc.Terms.make(1, 4)
+    with pytest.raises(ValueError):
+        sho.solve(A, t, orc.Terms.make(0, 8), 4, lambda v: v)
