@@ -52,6 +52,18 @@ def env_rank():
         int(os.environ.get("LOCAL_RANK", "0"))
 
 
+def ncu_traffic(kernel, m, n):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of ``kernel``
+    from the committed ``ncu --set full`` capture (profiles/traffic.json),
+    when it was taken on this exact per-rank shape; else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)[kernel]
+    except (OSError, KeyError, ValueError):
+        return None
+    return d["dram_bytes_per_launch"] if (d.get("m"), d.get("n")) == (m, n) else None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -219,35 +231,43 @@ def run_ours(args):
     m_loc = r1 - r0
     peaks, peaks_kind = measured_peaks()
     # ---------------- e2e: full solve from pinned host memory ----------------
-    A_pin = torch.from_numpy(prob.A).pin_memory()
-    prob_pin = gf.GraphFormProblem(A_pin, prob.f, prob.g)
-    e2e_runs = []
-    for _ in range(3):   # the first call warms module load / allocator; best of the rest
+    e2e = None
+    if not args.skip_e2e:
+        A_pin = torch.from_numpy(prob.A).pin_memory()
+        prob_pin = gf.GraphFormProblem(A_pin, prob.f, prob.g)
+        e2e_runs = []
+        for _ in range(3):   # the first call warms module load / allocator; best of the rest
+            sync()
+            t0 = time.perf_counter()
+            res = gf.solve(prob_pin, comm=comm)
+            torch.cuda.synchronize()
+            e2e_runs.append((max_over_ranks([time.perf_counter() - t0])[0], res))
+        e2e_time, res = min(e2e_runs[1:], key=lambda r: r[0]) if len(e2e_runs) > 1 else e2e_runs[-1]
+        # phase breakdown of the same public-API path (diagnostic, not the headline)
         sync()
         t0 = time.perf_counter()
-        res = gf.solve(prob_pin, comm=comm)
+        setup_b = gf.prepare(prob_pin, comm=comm)
         torch.cuda.synchronize()
-        e2e_runs.append((max_over_ranks([time.perf_counter() - t0])[0], res))
-    e2e_time, res = min(e2e_runs[1:], key=lambda r: r[0]) if len(e2e_runs) > 1 else e2e_runs[-1]
-    # phase breakdown of the same public-API path (diagnostic, not the headline)
-    sync()
-    t0 = time.perf_counter()
-    setup_b = gf.prepare(prob_pin, comm=comm)
-    torch.cuda.synchronize()
-    t1 = time.perf_counter()
-    run_b = slv._Run(setup_b, prob.f, prob.g, gf.SolverSettings(), None, None, m_loc)
-    torch.cuda.synchronize()
-    t2 = time.perf_counter()
-    run_b.run(0)
-    t3 = time.perf_counter()
-    run_b.result()
-    t4 = time.perf_counter()
-    phases = {"prepare_s": t1 - t0, "solver_create_s": t2 - t1, "iterate_s": t3 - t2, "result_s": t4 - t3,
-              "iterations": int(run_b.state.iterations)}
-    del run_b, setup_b
-    h2d = prob.A.nbytes + sum(getattr(prob.f, k).nbytes for k in "abcde") + m_loc \
-        + sum(getattr(prob.g, k).nbytes for k in "abcde") + n
-    d2h = 8 * (2 * m_loc + 2 * n)
+        t1 = time.perf_counter()
+        run_b = slv._Run(setup_b, prob.f, prob.g, gf.SolverSettings(), None, None, m_loc)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        run_b.run(0)
+        t3 = time.perf_counter()
+        run_b.result()
+        t4 = time.perf_counter()
+        phases = {"prepare_s": t1 - t0, "solver_create_s": t2 - t1, "iterate_s": t3 - t2, "result_s": t4 - t3,
+                  "iterations": int(run_b.state.iterations)}
+        del run_b, setup_b
+        h2d = prob.A.nbytes + sum(getattr(prob.f, k).nbytes for k in "abcde") + m_loc \
+            + sum(getattr(prob.g, k).nbytes for k in "abcde") + n
+        d2h = 8 * (2 * m_loc + 2 * n)
+        e2e = {"value": res.iterations / e2e_time, "unit": "iters/s",
+               "h2d_bytes_per_step": int(h2d / max(res.iterations, 1)),
+               "d2h_bytes_per_step": int(d2h / max(res.iterations, 1)),
+               "time_to_eps_s": e2e_time, "iterations": res.iterations, "status": res.status.value,
+               "objective": res.objective, "setup_s": res.setup_time, "h2d_bytes_total": int(h2d),
+               "runs_s": [round(r[0], 4) for r in e2e_runs], "phases": phases}
     # ---------------- device-resident iteration timing ----------------
     setup = gf.prepare(prob, comm=comm)
     tight = gf.SolverSettings(abs_tol=1e-12, rel_tol=1e-12, max_iter=args.warmup + 2 * args.steps + 8)
@@ -297,14 +317,9 @@ def run_ours(args):
                    "m": m, "n": n, "parallelism": f"row partition x{world}" + (" (NCCL all-reduce)" if use_comm else ""),
                    "rows_per_rank": m_loc,
                    "l2": "A is 4 GB >> 126 MB L2; no flush needed"},
-        "e2e": {"value": res.iterations / e2e_time, "unit": "iters/s",
-                "h2d_bytes_per_step": int(h2d / max(res.iterations, 1)),
-                "d2h_bytes_per_step": int(d2h / max(res.iterations, 1)),
-                "time_to_eps_s": e2e_time, "iterations": res.iterations, "status": res.status.value,
-                "objective": res.objective, "setup_s": res.setup_time, "h2d_bytes_total": int(h2d),
-                "runs_s": [round(r[0], 4) for r in e2e_runs], "phases": phases},
+        "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": dom,
+                     "frac": achieved / peak, "traffic": ncu_traffic(dom, m_loc, n), "kernel": dom,
                      "algorithmic_bytes_per_launch": alg_bytes, "peak_kind": peaks_kind},
         "kernels": kernels,
         "gpu_launches": int(l1.value - l0.value),
@@ -330,6 +345,8 @@ def main():
     ap.add_argument("--m", type=int, default=M_FULL)
     ap.add_argument("--n", type=int, default=N_FULL)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true",
+                    help="profiling runs only: skip the end-to-end solves (the line then has e2e null)")
     ap.add_argument("--force-comm", action="store_true",
                     help="use the NCCL row-partition path even on one GPU (checks the multi-GPU plumbing)")
     args = ap.parse_args()
