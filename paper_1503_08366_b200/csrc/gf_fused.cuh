@@ -35,10 +35,16 @@
 
 namespace gf {
 
-constexpr int kFusedThreads = 512;                 // compute threads
-constexpr int kFusedWarps = kFusedThreads / kWarp;
-constexpr int kFusedCTA = kFusedThreads + kWarp;   // + the epilogue warp
 constexpr int kMaxSlots = 32;
+// Epilogue warps: warp e takes the groups ge = e (mod kFusedEpi) and owns
+// hand-off buffer e, so each warp has kFusedEpi row-pass periods per group
+// while the latency from R(ge) to its weights stays under the two-period lag.
+// Three: 16 + 3 + 1 = 20 warps keeps 5 warps per SM sub-partition (96 registers
+// per thread); with 20 compute warps the CTA has 24 warps (80 registers).
+constexpr int kFusedEpiMax = 3;
+__host__ __device__ constexpr int fused_epi(int cw) { return 3; }
+// CTA size for CW compute warps: + the epilogue warps + 1 producer warp
+__host__ __device__ constexpr int fused_threads(int cw) { return (cw + fused_epi(cw) + 1) * 32; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -108,6 +114,8 @@ __device__ __forceinline__ void vaxpy(double2& acc, const double2& a, double w) 
 }
 
 struct FusedPlan {
+  int cw = 0;        // compute warps (template instance: 16 or 20)
+  int ne = 0;        // epilogue warps (= partial records per CTA)
   int nv = 0;        // 16-byte vectors per thread per row (template instance)
   int nslot = 0;     // rows resident in shared memory
   int tr = 0;        // rows per group (template instance: 1, 2 or 4)
@@ -120,7 +128,12 @@ inline FusedPlan plan_fused(int64_t m, int64_t ld, int esize, int sms, size_t sm
   FusedPlan p;
   const int vn = 16 / esize;
   const int64_t nvec = ld / vn;
-  p.nv = (int)ceil_div(nvec, kFusedThreads);
+  // 20 compute warps when that lowers the vectors per thread (shorter
+  // per-warp critical path per row; registers still fit at 736 threads)
+  const int nv16 = (int)ceil_div(nvec, 16 * 32), nv20 = (int)ceil_div(nvec, 20 * 32);
+  p.cw = (nv20 < nv16 && nv20 <= 4) ? 20 : 16;
+  p.nv = p.cw == 20 ? nv20 : nv16;
+  p.ne = fused_epi(p.cw);
   const size_t row_bytes = (size_t)ld * esize;
   const size_t budget = smem_max > 8192 ? smem_max - 8192 : 0;
   p.nslot = (int)std::min<size_t>(kMaxSlots, budget / row_bytes);
@@ -166,10 +179,12 @@ __device__ __forceinline__ T warp_multi_sum(T (&v)[K], int lane) {
   return r;
 }
 
-// Epi must provide: NR, active(), begin(), RowIn, load_in(i),
-// finish(i, in, dots, red, flags, w0, w1)   (YEpi in gf_solver.cu does).
+// Epi must provide: NR, active(), begin(), RowIn, load_in(i), Mid,
+// mid(in, dots, w0, w1) (the column-pass weights: critical path) and
+// tail(i, in, dots, mid, red, flags) (stores, reductions)  -- YEpi does.
 //
-// Warp roles (no CTA-wide barrier after setup; every hand-off is an mbarrier):
+// Warp roles (no CTA-wide barrier after setup; every hand-off is an mbarrier),
+// shown for CW = 16 compute warps:
 //   warps 0..15  compute   R(t): dots of group t -> red_s[t&1] (arrive redf)
 //                          C(t-2): column pass with w_s[t&1]  (wait wf, arrive we;
 //                          arrive sfree[slot] per row consumed)
@@ -179,12 +194,19 @@ __device__ __forceinline__ T warp_multi_sum(T (&v)[K], int lane) {
 //                          warps double the rows in flight through the serial
 //                          fp64 epilogue, which is latency- not throughput-bound.
 //   warp 18      producer  wait sfree[slot] -> TMA bulk copy of the row NSLOT ahead
-constexpr int kEpiWarp = kFusedWarps;        // 16 and 17
-constexpr int kProdWarp = kFusedWarps + 2;   // 18
-constexpr int kFusedAll = kFusedThreads + 3 * kWarp;
+// Dev instrumentation (tools/fused_bench.cu): per-CTA cycle counters of the
+// pipeline waits and epilogue phases; compiled out of the library.
+#ifdef GF_FUSED_TRACE
+__device__ unsigned long long gf_fused_trace[148 * 16];
+#define GF_TR_T0() const long long tr_t0_ = clock64()
+#define GF_TR_ADD(slot, t0) atomicAdd(&gf_fused_trace[blockIdx.x * 16 + (slot)], (unsigned long long)(clock64() - (t0)))
+#else
+#define GF_TR_T0() (void)0
+#define GF_TR_ADD(slot, t0) (void)0
+#endif
 
-template <typename T, int NV, int TR, class Epi>
-__global__ void __launch_bounds__(kFusedAll, 1)
+template <typename T, int NV, int TR, int CW, class Epi>
+__global__ void __launch_bounds__(fused_threads(CW), 1)
 fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* __restrict__ x0,
                     const T* __restrict__ x1, Epi epi, int nslot, double* __restrict__ rpart,
                     double* __restrict__ cpart) {
@@ -193,11 +215,17 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
   constexpr int NR = Epi::NR;
   constexpr int K = 2 * TR;
   constexpr int LGK = K == 2 ? 1 : (K == 4 ? 2 : 3);
+  constexpr int kFusedWarps = CW;
+  constexpr int kFusedThreads = CW * kWarp;
+  constexpr int NE = fused_epi(CW);
+  constexpr int kEpiWarp = CW;          // CW .. CW + NE - 1
+  constexpr int kProdWarp = CW + NE;
+  static_assert(CW <= 32, "one epilogue lane per compute warp");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxSlots], sfree[kMaxSlots];
-  __shared__ __align__(8) uint64_t redf[2], rede[2], wf[2], we[2];
-  __shared__ T red_s[2][kFusedWarps][K];
-  __shared__ T w_s[2][TR][2];
+  __shared__ __align__(8) uint64_t redf[NE], rede[NE], wf[NE], we[NE];
+  __shared__ T red_s[NE][kFusedWarps][K];
+  __shared__ T w_s[NE][TR][2];
 
   if (!epi.active()) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -213,7 +241,7 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
       mbar_init(&full[s], 1);
       mbar_init(&sfree[s], kFusedWarps);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NE; ++b) {
       mbar_init(&redf[b], kFusedWarps);
       mbar_init(&rede[b], 1);
       mbar_init(&wf[b], 1);
@@ -238,9 +266,9 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
     return;
   }
 
-  if (warp == kEpiWarp || warp == kEpiWarp + 1) {
+  if (warp >= kEpiWarp && warp < kEpiWarp + NE) {
     // ===================== epilogue warps =====================
-    const int par = warp - kEpiWarp;
+    const int par = warp - kEpiWarp;   // this warp's groups and buffer
     epi.begin();
     double ered[NR > 0 ? NR : 1];
 #pragma unroll
@@ -248,11 +276,19 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
     unsigned eflags = 0;
     typename Epi::RowIn in{};
     if (lane < TR && par * TR + lane < nr) in = epi.load_in(r0 + par * TR + lane);
-    for (int ge = par; ge < ng; ge += 2) {
-      const int b = ge & 1;
-      const unsigned use = (unsigned)(ge >> 1);
+    for (int ge = par; ge < ng; ge += NE) {
+      const int b = par;
+      const unsigned use = (unsigned)(ge / NE);
+#ifdef GF_FUSED_TRACE
+      long long c0 = clock64();
+#endif
       mbar_wait(&redf[b], use & 1u);
-      // fixed-order tree over the 16 compute warps: lanes 0..15 load one warp each
+#ifdef GF_FUSED_TRACE
+      long long c1 = clock64();
+      if (lane == 0) GF_TR_ADD(0, c0);
+#endif
+      // fixed-order tree over the CW compute warps: lane w loads warp w's partials
+      constexpr int RW = CW <= 16 ? 16 : 32;   // shuffle width covering the warps
       double v[K];
 #pragma unroll
       for (int q = 0; q < K; ++q) v[q] = lane < kFusedWarps ? (double)red_s[b][lane][q] : 0.0;
@@ -261,29 +297,50 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
 #pragma unroll
       for (int q = 0; q < K; ++q)
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o, 16);
-      if (ge >= 2) mbar_wait(&we[b], (use - 1) & 1u);     // w_s[b] consumed by C(ge-2)
+        for (int o = RW / 2; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o, RW);
+#ifdef GF_FUSED_TRACE
+      if (lane == 0) GF_TR_ADD(2, c1);
+      c1 = clock64();
+#endif
+      if (use >= 1) mbar_wait(&we[b], (use - 1) & 1u);    // w_s[b] consumed by C(ge-NE)
+#ifdef GF_FUSED_TRACE
+      if (lane == 0) GF_TR_ADD(3, c1);
+      c1 = clock64();
+#endif
       const int g = min(TR, nr - ge * TR);
-      if (lane < g) {
-        double dots[2] = {0.0, 0.0};
+      double dots[2] = {0.0, 0.0};
 #pragma unroll
-        for (int rr = 0; rr < TR; ++rr)
-          if (rr == lane) { dots[0] = v[2 * rr]; dots[1] = v[2 * rr + 1]; }
+      for (int rr = 0; rr < TR; ++rr)
+        if (rr == lane) { dots[0] = v[2 * rr]; dots[1] = v[2 * rr + 1]; }
+      // critical path first: the column-pass weights, handed off before the
+      // row's stores and reductions (Epi::tail) run
+      typename Epi::Mid md{};
+      if (lane < g) {
         double w0, w1;
-        epi.finish(r0 + (int64_t)ge * TR + lane, in, dots, ered, eflags, w0, w1);
+        md = epi.mid(in, dots, w0, w1);
         w_s[b][lane][0] = (T)w0;
         w_s[b][lane][1] = (T)w1;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(&wf[b], 0);
-      const int jn = (ge + 2) * TR + lane;   // prefetch the inputs of this warp's next group
+#ifdef GF_FUSED_TRACE
+      if (lane == 0) GF_TR_ADD(4, c1);
+      c1 = clock64();
+#endif
+      if (lane < g) epi.tail(r0 + (int64_t)ge * TR + lane, in, dots, md, ered, eflags);
+      const int jn = (ge + NE) * TR + lane;   // prefetch the inputs of this warp's next group
       if (lane < TR && jn < nr) in = epi.load_in(r0 + jn);
+#ifdef GF_FUSED_TRACE
+      __syncwarp();
+      if (lane == 0) GF_TR_ADD(5, c1);
+      if (lane == 0) GF_TR_ADD(6, c0);
+#endif
     }
 #pragma unroll
     for (int k = 0; k < NR; ++k) ered[k] = warp_sum(ered[k]);
     eflags = warp_or(eflags);
-    if (lane == 0) {   // one partial record per epilogue warp: rpart[2 * cta + par]
-      double* out = rpart + (2 * (int64_t)blockIdx.x + par) * (NR + 1);
+    if (lane == 0) {   // one partial record per epilogue warp: rpart[NE * cta + par]
+      double* out = rpart + (NE * (int64_t)blockIdx.x + par) * (NR + 1);
       for (int k = 0; k < NR; ++k) out[k] = ered[k];
       out[NR] = (double)eflags;
     }
@@ -317,7 +374,13 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
         s[2 * rr] = 0;
         s[2 * rr + 1] = 0;
         if (jR < nr) {
+#ifdef GF_FUSED_TRACE
+          long long c0 = clock64();
+#endif
           mbar_wait(&full[slotR], phaseR);
+#ifdef GF_FUSED_TRACE
+          if (tid == 0) GF_TR_ADD(8, c0);
+#endif
           const V* row = reinterpret_cast<const V*>(smem_raw + slotR * rb);
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
@@ -332,17 +395,29 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
         }
       }
       const T tot = warp_multi_sum<K>(s, lane);   // lane (q << (5-LGK)) holds value q
-      const int b = t & 1;
-      const unsigned use = (unsigned)(t >> 1);
+      const int b = t % NE;
+      const unsigned use = (unsigned)(t / NE);
+#ifdef GF_FUSED_TRACE
+      long long c0 = clock64();
+#endif
       if (use >= 1) mbar_wait(&rede[b], (use - 1) & 1u);
+#ifdef GF_FUSED_TRACE
+      if (tid == 0) GF_TR_ADD(9, c0);
+#endif
       if ((lane & ((32 >> LGK) - 1)) == 0) red_s[b][warp][lane >> (5 - LGK)] = tot;
       __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(&redf[b], 0);
     }
     if (t >= 2) {   // ---- C(t-2) ----
-      const int b = t & 1;
-      const unsigned use = (unsigned)((t - 2) >> 1);
+      const int b = (t - 2) % NE;
+      const unsigned use = (unsigned)((t - 2) / NE);
+#ifdef GF_FUSED_TRACE
+      long long c0 = clock64();
+#endif
       mbar_wait(&wf[b], use & 1u);
+#ifdef GF_FUSED_TRACE
+      if (tid == 0) GF_TR_ADD(10, c0);
+#endif
       T w0[TR], w1[TR];
 #pragma unroll
       for (int rr = 0; rr < TR; ++rr) { w0[rr] = w_s[b][rr][0]; w1[rr] = w_s[b][rr][1]; }

@@ -98,40 +98,54 @@ struct YEpi {
                         double& w1) const {
     finish(i, load_in(i), dots, red, flags, w0, w1);
   }
+  // The fused kernel splits the epilogue at the column-pass weights: mid()
+  // is the critical path (the compute warps wait for w0, w1), tail() the
+  // stores and reductions that run after the hand-off.
+  struct Mid {
+    int64_t k;
+    double ykv, ytv, yh, yhh, nu, cyn;
+  };
+  __device__ Mid mid(const RowIn& in, const double* dots, double& w0, double& w1) const {
+    const bool cached = k_ >= 0;
+    Mid r;
+    r.k = cached ? k_ : ctl->k;
+    const double rho = cached ? rho_ : ctl->rho;
+    if (r.k == 0) {
+      r.ykv = warm_x ? dots[0] : in.yk;
+      r.ytv = in.yt;
+    } else {
+      r.ykv = dots[0];                        // y+ = A_hat x+  (projection.py:122)
+      r.ytv = M_(S_(in.cy, r.ykv), cached ? ratio_ : ctl->ratio);   // y~ + r_y - y+, rescaled (solver.py:420, :237)
+    }
+    const double di = in.di;
+    r.yh = prox_term(in.t, M_(rho, M_(di, di)), D_(S_(r.ykv, r.ytv), di));  // solver.py:331-336
+    r.yhh = M_(r.yh, di);
+    r.nu = M_(-rho, A_(S_(r.yhh, r.ykv), r.ytv));                            // solver.py:180
+    const double ry = A_(M_(alpha, r.yhh), M_(S_(1.0, alpha), r.ykv));      // solver.py:394
+    r.cyn = A_(ry, r.ytv);
+    w0 = r.cyn;
+    w1 = r.nu;
+    return r;
+  }
+  __device__ void tail(int64_t i, const RowIn& in, const double* dots, const Mid& r, double* red,
+                       unsigned& flags) const {
+    if (!isfinite(r.ykv)) flags |= kBadYPlus;
+    if (!isfinite(r.yh)) flags |= kBadYHalf;
+    const int64_t b = (r.k & 1) * m;
+    yk[i] = r.ykv;
+    yt[i] = r.ytv;
+    yh2[b + i] = r.yh;
+    nuh2[b + i] = r.nu;
+    cy[i] = r.cyn;
+    const double rp = S_(D_(dots[1], in.di), r.yh);   // (A x_1/2 - y_1/2)_i via A_hat
+    red[0] += rp * rp;
+    red[1] += r.yh * r.yh;
+    red[2] += eval_term(in.t, r.yh);
+    red[3] += (r.yhh - r.ykv) * (r.yhh - r.ykv);
+  }
   __device__ void finish(int64_t i, const RowIn& in, const double* dots, double* red, unsigned& flags,
                          double& w0, double& w1) const {
-    const bool cached = k_ >= 0;
-    const int64_t k = cached ? k_ : ctl->k;
-    const double rho = cached ? rho_ : ctl->rho;
-    double ykv, ytv;
-    if (k == 0) {
-      ykv = warm_x ? dots[0] : in.yk;
-      ytv = in.yt;
-    } else {
-      ykv = dots[0];                          // y+ = A_hat x+  (projection.py:122)
-      ytv = M_(S_(in.cy, ykv), cached ? ratio_ : ctl->ratio);   // y~ + r_y - y+, rescaled (solver.py:420, :237)
-    }
-    if (!isfinite(ykv)) flags |= kBadYPlus;
-    const double di = in.di;
-    const Term& t = in.t;
-    const double yh = prox_term(t, M_(rho, M_(di, di)), D_(S_(ykv, ytv), di));  // solver.py:331-336
-    if (!isfinite(yh)) flags |= kBadYHalf;
-    const double yhh = M_(yh, di);
-    const double nu = M_(-rho, A_(S_(yhh, ykv), ytv));                   // solver.py:180
-    const double ry = A_(M_(alpha, yhh), M_(S_(1.0, alpha), ykv));      // solver.py:394
-    const int64_t b = (k & 1) * m;
-    yk[i] = ykv;
-    yt[i] = ytv;
-    yh2[b + i] = yh;
-    nuh2[b + i] = nu;
-    cy[i] = A_(ry, ytv);
-    w0 = A_(ry, ytv);
-    w1 = nu;
-    const double rp = S_(D_(dots[1], di), yh);   // (A x_1/2 - y_1/2)_i via A_hat
-    red[0] += rp * rp;
-    red[1] += yh * yh;
-    red[2] += eval_term(t, yh);
-    red[3] += (yhh - ykv) * (yhh - ykv);
+    tail(i, in, dots, mid(in, dots, w0, w1), red, flags);
   }
 };
 
@@ -676,37 +690,47 @@ static YEpi<T> make_yepi(gf_solver* s) {
 }
 
 // attr_only: set the dynamic shared-memory limit of the instance (at create)
-template <typename T, int NV, int TR>
+template <typename T, int NV, int TR, int CW>
 static void fused_go(gf_solver* s, cudaStream_t st, bool attr_only) {
   const FusedPlan& p = s->fplan;
-  auto kern = fused_rowcol_kernel<T, NV, TR, YEpi<T>>;
+  auto kern = fused_rowcol_kernel<T, NV, TR, CW, YEpi<T>>;
   if (attr_only) {
     GF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
     return;
   }
-  kern<<<p.grid, kFusedAll, p.smem, st>>>((const T*)s->S->A->data, s->m, s->ld, s->xk_T.as<T>(), s->xh_T.as<T>(),
-                                          make_yepi<T>(s), p.nslot, s->rpart.as<double>(), s->cpart.as<double>());
+  kern<<<p.grid, fused_threads(CW), p.smem, st>>>((const T*)s->S->A->data, s->m, s->ld, s->xk_T.as<T>(),
+                                                  s->xh_T.as<T>(), make_yepi<T>(s), p.nslot,
+                                                  s->rpart.as<double>(), s->cpart.as<double>());
   GF_CHECK_LAUNCH();
 }
 
-template <typename T, int NV>
+template <typename T, int NV, int CW>
 static void fused_tr(gf_solver* s, cudaStream_t st, bool attr_only) {
   switch (s->fplan.tr) {
-    case 4: fused_go<T, NV, 4>(s, st, attr_only); break;
-    case 2: fused_go<T, NV, 2>(s, st, attr_only); break;
-    default: fused_go<T, NV, 1>(s, st, attr_only); break;
+    case 4: fused_go<T, NV, 4, CW>(s, st, attr_only); break;
+    case 2: fused_go<T, NV, 2, CW>(s, st, attr_only); break;
+    default: fused_go<T, NV, 1, CW>(s, st, attr_only); break;
   }
 }
 
+// plan_fused picks 20 compute warps only for NV in {2, 3, 4}
 template <typename T>
 static void fused_dispatch(gf_solver* s, cudaStream_t st, bool attr_only) {
+  if (s->fplan.cw == 20) {
+    switch (s->fplan.nv) {
+      case 2: fused_tr<T, 2, 20>(s, st, attr_only); break;
+      case 3: fused_tr<T, 3, 20>(s, st, attr_only); break;
+      default: fused_tr<T, 4, 20>(s, st, attr_only); break;
+    }
+    return;
+  }
   switch (s->fplan.nv) {
-    case 1: fused_tr<T, 1>(s, st, attr_only); break;
-    case 2: fused_tr<T, 2>(s, st, attr_only); break;
-    case 3: fused_tr<T, 3>(s, st, attr_only); break;
-    case 4: fused_tr<T, 4>(s, st, attr_only); break;
-    case 5: fused_tr<T, 5>(s, st, attr_only); break;
-    default: fused_tr<T, 6>(s, st, attr_only); break;
+    case 1: fused_tr<T, 1, 16>(s, st, attr_only); break;
+    case 2: fused_tr<T, 2, 16>(s, st, attr_only); break;
+    case 3: fused_tr<T, 3, 16>(s, st, attr_only); break;
+    case 4: fused_tr<T, 4, 16>(s, st, attr_only); break;
+    case 5: fused_tr<T, 5, 16>(s, st, attr_only); break;
+    default: fused_tr<T, 6, 16>(s, st, attr_only); break;
   }
 }
 
@@ -771,7 +795,7 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
       launch_fused<T>(s, st);
       s->mark(7, st, false);
       slabs = s->fplan.grid;
-      nrpart = 2 * s->fplan.grid;   // one record per epilogue warp
+      nrpart = s->fplan.ne * s->fplan.grid;   // one record per epilogue warp
       s->launches += 1;
     } else {             // two passes: row pass (+ y side), then column pass
       s->mark(1, st, true);
@@ -970,7 +994,7 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
     }
   }
   const int64_t nslab = std::max<int64_t>(s->cplan.slabs, s->fplan.ok ? s->fplan.grid : 1);
-  vec(s->rpart, std::max<int64_t>(s->grid_r, s->fplan.ok ? 2 * s->fplan.grid : 1) * (kRedY + 1));
+  vec(s->rpart, std::max<int64_t>(s->grid_r, s->fplan.ok ? kFusedEpiMax * s->fplan.grid : 1) * (kRedY + 1));
   vec(s->xpart, s->grid_s * (kRedX + 1));
   vec(s->zpart, s->grid_z);
   vec(s->red, 2 * s->ld + kScal);
