@@ -76,6 +76,8 @@ typedef struct {
   double delta, tau;
   int projection;
   double projection_tol; /* <= 0: the decreasing schedule (solver.py:398-406) */
+  int gap_stop;          /* solver.py:378-390: also stop on the duality gap at the
+                            full iterate (problem.py:67-85) */
 } gf_settings;
 
 /* Per-iteration scalars handed to callbacks (solver.py:359-360) and the
@@ -89,6 +91,8 @@ typedef struct {
   double objective;
   double final_rho;        /* SolveResult.final_rho                     */
   int64_t inner_iterations;/* CGLS inner iterations of iteration k      */
+  double gap;              /* SolveResult.gap of the last gap test       */
+  int gap_valid;           /* 0: no gap (gap_stop off or a conjugate unsupported) */
 } gf_solver_state;
 
 typedef struct {
@@ -115,6 +119,12 @@ int gf_prox_base(int64_t n, int kind, const double* rho, const double* v,
 int gf_evaluate(const gf_terms* t, const double* v, double* result, void* stream);
 /* functions.py:160-164 eval_base, elementwise (DEVICE pointers). */
 int gf_eval_base(int64_t n, int kind, const double* x, double* out, void* stream);
+/* functions.py:147-150 conjugate_base: h*(w) elementwise (DEVICE pointers). */
+int gf_conj_base(int64_t n, int kind, const double* w, double* out, void* stream);
+/* functions.py:329-365 SeparableFunction.conjugate: sum_i f_i*(w_i) -> *result
+ * (host); *supported = 0 when some term has e > 0 and a kind without a closed
+ * form (the reference returns None).  Term and w pointers DEVICE. */
+int gf_conjugate(const gf_terms* t, const double* w, double* result, int* supported, void* stream);
 
 /* ------------------------------------------------------------ matrices -- */
 /* problem.py:30-49 (coercion of A): copy an m x n row-major matrix

@@ -196,6 +196,100 @@ def evaluate(t: Terms, v) -> float:
     return float(t.c @ hv) + float(t.d @ v) + 0.5 * float(t.e @ (v * v))
 
 
+# ---------------------------------------------------------- conjugates ----
+def conj_kind(code: int, w):
+    """h*(w) elementwise, +inf off-domain (functions.py:108-144)."""
+    w = np.asarray(w, float)
+    with np.errstate(invalid="ignore", divide="ignore", over="ignore"):
+        if code == ZERO:
+            return np.where(w == 0.0, 0.0, np.inf)
+        if code == ABS:
+            return np.where(np.abs(w) <= 1.0, 0.0, np.inf)
+        if code == SQUARE:
+            return 0.5 * w * w
+        if code == HUBER:
+            return np.where(np.abs(w) <= 1.0, 0.5 * w * w, np.inf)
+        if code == NEG_ENTR:
+            return np.exp(w - 1.0)
+        if code == LOGISTIC:
+            out = np.full_like(w, np.inf)
+            ok = (w >= 0.0) & (w <= 1.0)
+            wk = w[ok]
+            lhs = np.where(wk > 0.0, wk * np.log(np.where(wk > 0.0, wk, 1.0)), 0.0)
+            rhs = np.where(wk < 1.0, (1.0 - wk) * np.log1p(-np.where(wk < 1.0, wk, 0.0)), 0.0)
+            out[ok] = lhs + rhs
+            return out
+        if code == MAX_POS0:
+            return np.where((w >= 0.0) & (w <= 1.0), 0.0, np.inf)
+        if code == IND_GE0:
+            return np.where(w <= 0.0, 0.0, np.inf)
+        if code == IND_LE0:
+            return np.where(w >= 0.0, 0.0, np.inf)
+        if code == IND_EQ0:
+            return np.zeros_like(w)
+    raise ValueError(code)
+
+
+_EPOS_OK = (ZERO, SQUARE, IND_EQ0, IND_GE0, IND_LE0)   # functions.py:182-190
+
+
+def conjugate(t: Terms, w):
+    """sum_i f_i*(w_i), or None when a term with e > 0 has no closed form
+    (functions.py:329-393)."""
+    w = np.asarray(w, float)
+    zc = t.c == 0.0
+    codes = np.where(zc, ZERO, t.h)
+    c = np.where(zc, 1.0, t.c)
+    a, b, e = t.a, t.b, t.e
+    wd = w - t.d
+    vals = np.empty_like(w)
+    with np.errstate(invalid="ignore", over="ignore", divide="ignore"):
+        for code in np.unique(codes):
+            sel = codes == code
+            s0 = sel & (e == 0.0)
+            sp = sel & (e != 0.0)
+            if s0.any():
+                q = wd[s0] / (a[s0] * c[s0])
+                vals[s0] = c[s0] * conj_kind(int(code), q) + b[s0] * wd[s0] / a[s0]
+            if sp.any():
+                if int(code) not in _EPOS_OK:
+                    return None
+                wq, aq, bq, cq, eq = wd[sp], a[sp], b[sp], c[sp], e[sp]
+                if code == ZERO:
+                    vals[sp] = wq * wq / (2.0 * eq)
+                elif code == SQUARE:
+                    alpha = cq * aq * aq + eq
+                    beta = -cq * aq * bq
+                    cst = 0.5 * cq * bq * bq
+                    tt = wq - beta
+                    vals[sp] = tt * tt / (2.0 * alpha) - cst
+                else:
+                    x0 = bq / aq
+                    boundary = wq * x0 - 0.5 * eq * x0 * x0
+                    if code == IND_EQ0:
+                        vals[sp] = boundary
+                    else:
+                        xbar = wq / eq
+                        interior = wq * wq / (2.0 * eq)
+                        if code == IND_GE0:
+                            feas = np.where(aq > 0.0, xbar >= x0, xbar <= x0)
+                        else:
+                            feas = np.where(aq > 0.0, xbar <= x0, xbar >= x0)
+                        vals[sp] = np.where(feas, interior, boundary)
+    return float(np.sum(vals))
+
+
+def duality_gap(f: Terms, g: Terms, x, y, mu, nu):
+    """f(y) + f*(nu) + g(x) + g*(mu), None if unsupported (problem.py:67-85)."""
+    fc = conjugate(f, nu)
+    if fc is None:
+        return None
+    gc = conjugate(g, mu)
+    if gc is None:
+        return None
+    return evaluate(f, y) + fc + evaluate(g, x) + gc
+
+
 # ------------------------------------------------------- equilibration ----
 def _sq_rows(A, w, chunk=256):
     """(A∘A) w, formed chunk by chunk (equilibration.py:94-116)."""
@@ -341,7 +435,7 @@ def project_indirect(P: Projector, c, d, x_warm=None, y_warm=None, tol=None):
 DEFAULTS = dict(rho0=1.0, abs_tol=1e-4, rel_tol=1e-3, max_iter=10_000,
                 alpha=1.7, adaptive_rho=True, delta=1.05, tau=0.8,
                 equilibrate=True, projection="direct", projection_tol=None,
-                max_inner=None)
+                max_inner=None, gap_stop=False)
 
 
 def prepare(A, settings=None, scaling=None):
@@ -395,6 +489,7 @@ def solve(A, f: Terms, g: Terms, settings=None, x0=None, nu0=None,
     xh, yh, muh, nuh = np.zeros(n), np.zeros(m), np.zeros(n), np.zeros(m)
     obj = evaluate(f, yh) + evaluate(g, xh)
     r_pri = r_dual = float("inf")
+    gap = None
     hist = []
     indirect = s["projection"] == "indirect"
     for k in range(s["max_iter"]):
@@ -422,6 +517,15 @@ def solve(A, f: Terms, g: Terms, settings=None, x0=None, nu0=None,
         if r_pri <= eps_pri and r_dual <= eps_dual:
             status, iters = "Solved", k + 1
             break
+        if s["gap_stop"]:                                # solver.py:378-390
+            xf, yf = e * xk, yk / d
+            muf, nuf = -rho * xt / e, -rho * d * yt
+            gap = duality_gap(f, g, xf, yf, muf, nuf)
+            if gap is not None and np.isfinite(gap):
+                objf = evaluate(f, yf) + evaluate(g, xf)
+                if np.isfinite(objf) and gap <= s["abs_tol"] + s["rel_tol"] * abs(objf):
+                    status, iters = "Solved", k + 1
+                    break
         rx = alpha * xhh + (1.0 - alpha) * xk
         ry = alpha * yhh + (1.0 - alpha) * yk
         cx, cy = rx + xt, ry + yt
@@ -454,5 +558,5 @@ def solve(A, f: Terms, g: Terms, settings=None, x0=None, nu0=None,
                 rho, lo_mark = new, k
                 xt, yt = xt * ratio, yt * ratio
     return dict(x=xh, y=yh, mu=muh, nu=nuh, objective=obj, r_pri=r_pri,
-                r_dual=r_dual, status=status, iterations=iters, final_rho=rho,
+                r_dual=r_dual, status=status, iterations=iters, final_rho=rho, gap=gap,
                 history=np.array(hist, float).reshape(-1, 6), setup=setup)

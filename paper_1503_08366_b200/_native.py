@@ -40,14 +40,15 @@ class Settings(C.Structure):
     _fields_ = [("rho0", C.c_double), ("abs_tol", C.c_double), ("rel_tol", C.c_double),
                 ("max_iter", C.c_int64), ("alpha", C.c_double), ("adaptive_rho", C.c_int),
                 ("delta", C.c_double), ("tau", C.c_double), ("projection", C.c_int),
-                ("projection_tol", C.c_double)]
+                ("projection_tol", C.c_double), ("gap_stop", C.c_int)]
 
 
 class SolverState(C.Structure):
     _fields_ = [("status", C.c_int), ("iterations", C.c_int64), ("k", C.c_int64),
                 ("r_pri", C.c_double), ("r_dual", C.c_double), ("eps_pri", C.c_double),
                 ("eps_dual", C.c_double), ("rho", C.c_double), ("objective", C.c_double),
-                ("final_rho", C.c_double), ("inner_iterations", C.c_int64)]
+                ("final_rho", C.c_double), ("inner_iterations", C.c_int64),
+                ("gap", C.c_double), ("gap_valid", C.c_int)]
 
 
 class SetupInfo(C.Structure):
@@ -64,6 +65,8 @@ _SIGS = {
     "gf_prox_base": ([C.c_int64, C.c_int, _P, _P, _P, _P], C.c_int),
     "gf_evaluate": ([C.POINTER(Terms), _P, c_double_p, _P], C.c_int),
     "gf_eval_base": ([C.c_int64, C.c_int, _P, _P, _P], C.c_int),
+    "gf_conj_base": ([C.c_int64, C.c_int, _P, _P, _P], C.c_int),
+    "gf_conjugate": ([C.POINTER(Terms), _P, c_double_p, c_int_p, _P], C.c_int),
     "gf_matrix_create": ([C.c_int, C.c_int64, C.c_int64, _P, C.c_int, C.c_int64, _P, C.POINTER(_P)], C.c_int),
     "gf_matrix_destroy": ([_P], C.c_int),
     "gf_matrix_shape": ([_P, c_int64_p, c_int64_p, c_int64_p, c_int_p], C.c_int),
@@ -249,6 +252,31 @@ def evaluate(sf, v) -> float:
     out = C.c_double()
     check(L.gf_evaluate(C.byref(T), ptr(v_t), C.byref(out), stream()))
     return float(out.value)
+
+
+def conjugate(sf, w):
+    """Sum of the term conjugates at w, or None when unsupported."""
+    L = lib()
+    w_t = to_device64(w)
+    if w_t.dim() != 1 or w_t.numel() != len(sf):
+        raise DimensionError(f"expected vector of length {len(sf)}, got shape {tuple(np.shape(w))}")
+    T, keep = device_terms(sf)
+    out = C.c_double()
+    ok = C.c_int()
+    check(L.gf_conjugate(C.byref(T), ptr(w_t), C.byref(out), C.byref(ok), stream()))
+    return float(out.value) if ok.value else None
+
+
+def conj_base(code, w):
+    import torch
+    L = lib()
+    scalar = np.ndim(w) == 0 and not is_torch(w)
+    w_t = to_device64(np.atleast_1d(np.asarray(w, float)) if scalar else w)
+    out = torch.empty_like(w_t)
+    check(L.gf_conj_base(w_t.numel(), int(code), ptr(w_t), ptr(out), stream()))
+    if scalar:
+        return float(out.item())
+    return like_input(out, w)
 
 
 def eval_base(code, x):

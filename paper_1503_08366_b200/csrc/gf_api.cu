@@ -273,6 +273,24 @@ int gf_eval_base(int64_t n, int kind, const double* x, double* out, void* stream
   });
 }
 
+int gf_conj_base(int64_t n, int kind, const double* w, double* out, void* stream) {
+  return guarded([&] {
+    GF_REQUIRE(kind >= 0 && kind <= 9, GF_E_PARAMETER, "unknown base function code");
+    conj_base(kind, n, w, out, (cudaStream_t)stream);
+    GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  });
+}
+
+int gf_conjugate(const gf_terms* t, const double* w, double* result, int* supported, void* stream) {
+  return guarded([&] {
+    check_terms(t);
+    TermsView view{t->h, t->a, t->b, t->c, t->d, t->e};
+    bool ok = true;
+    *result = conjugate(view, t->n, w, &ok, (cudaStream_t)stream);
+    *supported = ok ? 1 : 0;
+  });
+}
+
 int gf_matrix_create(int dtype, int64_t m, int64_t n, const void* src, int src_dtype, int64_t src_ld, void* stream,
                      gf_matrix** out) {
   return guarded([&] {

@@ -96,6 +96,9 @@ void prox_separable(const TermsView& t, int64_t n, const double* rho, const doub
 void prox_base(int kind, int64_t n, const double* rho, const double* v, double* out, cudaStream_t st);
 double evaluate(const TermsView& t, int64_t n, const double* v, cudaStream_t st);
 void eval_base(int kind, int64_t n, const double* x, double* out, cudaStream_t st);
+void conj_base(int kind, int64_t n, const double* w, double* out, cudaStream_t st);
+double conjugate(const TermsView& t, int64_t n, const double* w, bool* supported, cudaStream_t st);
+bool conj_supported(const TermsView& t, int64_t n, cudaStream_t st);
 
 // ------------------------------------------------- CGLS indirect (gf_cgls) --
 int64_t cgls_solve(const gf_matrix* A, bool tall, gf_comm* comm, const double* h1, const double* h2, double* z,

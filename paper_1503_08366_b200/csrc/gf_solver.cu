@@ -43,17 +43,24 @@ struct Ctl {
   int64_t inner;       // CGLS inner iterations of the last projection
   double rho, rho_prev, ratio, final_rho;
   double r_pri, r_dual, eps_pri, eps_dual, objective;
+  double gap;          // duality gap of the last gap test (solver.py:378-390)
+  int64_t gap_set;     // 1 once a gap was computed
 };
 
 struct Params {
   double abs_tol, rel_tol, alpha, delta, tau;
   int64_t max_iter;
   int adaptive;
+  int gap;             // gap-based stopping on (and every conjugate supported)
 };
 
-constexpr int kRedY = 4;  // r_pri^2, ||y||^2, f(y), drift_y^2 (+ flags)
-constexpr int kRedX = 3;  // ||mu||^2, g(x), drift_x^2 (+ flags)
-constexpr int kScal = 6;  // all-reduced scalars after the 2*ld column sums
+// per-row / per-column reductions (+ a flags word):
+//   y: r_pri^2, ||y||^2, f(y), drift_y^2, f(y_full), f*(nu_full)
+//   x: ||mu||^2, g(x), drift_x^2, g(x_full), g*(mu_full)
+// the last two of each are the duality gap at the full iterate (gap_stop only)
+constexpr int kRedY = 6;
+constexpr int kRedX = 5;
+constexpr int kScal = 8;  // all-reduced scalars after the 2*ld column sums
 enum : unsigned { kBadXPlus = 1, kBadXHalf = 2, kBadYPlus = 4, kBadYHalf = 8 };
 
 template <typename T>
@@ -66,6 +73,7 @@ struct YEpi {
   int64_t m;
   double alpha;
   int warm_x;
+  int gap;
   // controller scalars, cached in registers by begin() (fused kernel)
   int64_t k_ = -1;
   double rho_ = 0.0, ratio_ = 1.0;
@@ -103,13 +111,14 @@ struct YEpi {
   // stores and reductions that run after the hand-off.
   struct Mid {
     int64_t k;
-    double ykv, ytv, yh, yhh, nu, cyn;
+    double rho, ykv, ytv, yh, yhh, nu, cyn;
   };
   __device__ Mid mid(const RowIn& in, const double* dots, double& w0, double& w1) const {
     const bool cached = k_ >= 0;
     Mid r;
     r.k = cached ? k_ : ctl->k;
     const double rho = cached ? rho_ : ctl->rho;
+    r.rho = rho;
     if (r.k == 0) {
       r.ykv = warm_x ? dots[0] : in.yk;
       r.ytv = in.yt;
@@ -142,6 +151,11 @@ struct YEpi {
     red[1] += r.yh * r.yh;
     red[2] += eval_term(in.t, r.yh);
     red[3] += (r.yhh - r.ykv) * (r.yhh - r.ykv);
+    if (gap) {   // full iterate y = y^ / d, nu = -rho d y~ (solver.py:379-382)
+      bool unsup = false;
+      red[4] += eval_term(in.t, D_(r.ykv, in.di));
+      red[5] += conj_term(in.t, M_(M_(-r.rho, in.di), r.ytv), unsup);
+    }
   }
   __device__ void finish(int64_t i, const RowIn& in, const double* dots, double* red, unsigned& flags,
                          double& w0, double& w1) const {
@@ -160,6 +174,7 @@ struct XEpi {
   int64_t n;
   double alpha;
   int wide;          // wide orientation: the first right-hand side is c_x
+  int gap;
   __device__ bool active() const { return ctl->status == GF_STATUS_RUNNING; }
   // init: x^, x~ given (warm start or zero) -- iteration 0 has no dual step.
   __device__ void apply(int64_t j, double xkv, double xtv, double* red, unsigned& flags) const {
@@ -184,6 +199,11 @@ struct XEpi {
     red[0] += mo * mo;
     red[1] += eval_term(t, xh);
     red[2] += (xhh - xkv) * (xhh - xkv);
+    if (gap) {   // full iterate x = e x^, mu = -rho x~ / e (solver.py:379-382)
+      bool unsup = false;
+      red[3] += eval_term(t, M_(ej, xkv));
+      red[4] += conj_term(t, D_(M_(-rho, xtv), ej), unsup);
+    }
   }
   __device__ void row(int64_t j, const double* dots, double* red, unsigned& flags) const {
     const double xp = dots[0];                                           // x+ (projection.py:121)
@@ -207,6 +227,7 @@ struct YEpiW {
   T* rhs_T;
   int64_t m;
   double alpha;
+  int gap;
   __device__ bool active() const { return ctl->status == GF_STATUS_RUNNING; }
   __device__ void row(int64_t i, const double* dots, double* red, unsigned& flags) const {
     const int64_t k = ctl->k;
@@ -239,6 +260,11 @@ struct YEpiW {
     red[1] += yh * yh;
     red[2] += eval_term(t, yh);
     red[3] += (yhh - ykv) * (yhh - ykv);
+    if (gap) {
+      bool unsup = false;
+      red[4] += eval_term(t, D_(ykv, di));
+      red[5] += conj_term(t, M_(M_(-rho, di), ytv), unsup);
+    }
   }
 };
 
@@ -265,7 +291,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) x_wide_kernel(XEpi<T> epi, const double* __restrict__ aw,
                                                      double* __restrict__ part, int sub) {
   if (!epi.active()) return;
-  double red[kRedX] = {0.0, 0.0, 0.0};
+  double red[kRedX] = {};
   unsigned flags = 0;
   const double ratio = epi.ctl->ratio;
   for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < epi.n; j += (int64_t)gridDim.x * blockDim.x) {
@@ -300,7 +326,7 @@ __global__ void __launch_bounds__(256) x_wide_kernel(XEpi<T> epi, const double* 
 
 template <typename T>
 __global__ void __launch_bounds__(256) x_init_kernel(XEpi<T> epi, double* __restrict__ part) {
-  double red[kRedX] = {0.0, 0.0, 0.0};
+  double red[kRedX] = {};
   unsigned flags = 0;
   for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < epi.n; j += (int64_t)gridDim.x * blockDim.x)
     epi.apply(j, epi.xk[j], epi.xt[j], red, flags);
@@ -328,8 +354,8 @@ __global__ void __launch_bounds__(256) x_init_kernel(XEpi<T> epi, double* __rest
   }
 }
 
-// Z1 scalars: reduce the R partials -> red[2*ld .. 2*ld+6):
-//   [r_pri^2, ||y||^2, f(y), drift_y^2, #bad y+, #bad y_1/2]
+// Z1 scalars: reduce the R partials -> red[2*ld .. 2*ld+8):
+//   [r_pri^2, ||y||^2, f(y), drift_y^2, #bad y+, #bad y_1/2, f(y_full), f*(nu_full)]
 __global__ void y_scalars_kernel(const double* __restrict__ rpart, int64_t count, double* __restrict__ out,
                                  const Ctl* ctl) {
   if (ctl->status != GF_STATUS_RUNNING) return;
@@ -344,7 +370,7 @@ __global__ void y_scalars_kernel(const double* __restrict__ rpart, int64_t count
       if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
       __syncthreads();
     }
-    if (threadIdx.x == 0) out[k] = sh[0];
+    if (threadIdx.x == 0) out[k < 4 ? k : k + 2] = sh[0];
     __syncthreads();
   }
   unsigned f = 0;
@@ -357,6 +383,19 @@ __global__ void y_scalars_kernel(const double* __restrict__ rpart, int64_t count
     out[4] = (t & kBadYPlus) ? 1.0 : 0.0;
     out[5] = (t & kBadYHalf) ? 1.0 : 0.0;
   }
+}
+
+// Gap-based stopping at the full iterate (solver.py:205-218, :378-390):
+// gap = ((f(y) + f*(nu)) + g(x)) + g*(mu) (problem.py:85); an infinite gap or
+// objective never stops.
+__device__ bool gap_test(Ctl* ctl, const Params& prm, const double* ys, const double* xs) {
+  const double gap = A_(A_(A_(ys[6], ys[7]), xs[3]), xs[4]);
+  ctl->gap = gap;
+  ctl->gap_set = 1;
+  if (!isfinite(gap)) return false;
+  const double obj = A_(ys[6], xs[3]);
+  if (!isfinite(obj)) return false;
+  return gap <= A_(prm.abs_tol, M_(prm.rel_tol, fabs(obj)));
 }
 
 // Z2: per column the projection right-hand side (tall) or x+ (wide) and the
@@ -471,7 +510,7 @@ control_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ red
     ctl->last_good = k;
     ctl->r_pri = r_pri; ctl->r_dual = r_dual; ctl->eps_pri = eps_pri; ctl->eps_dual = eps_dual;
     ctl->objective = obj;
-    if (r_pri <= eps_pri && r_dual <= eps_dual) {
+    if ((r_pri <= eps_pri && r_dual <= eps_dual) || (prm.gap && gap_test(ctl, prm, ys, xs))) {
       ctl->status = GF_STATUS_SOLVED;
       ctl->iterations = k + 1;
       ctl->final_rho = rho;
@@ -533,7 +572,8 @@ control_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ red
   ctl->last_good = k;
   ctl->r_pri = r_pri; ctl->r_dual = r_dual; ctl->eps_pri = eps_pri; ctl->eps_dual = eps_dual;
   ctl->objective = obj;
-  if (r_pri <= eps_pri && r_dual <= eps_dual) {   // solver.py:201, :373-376
+  if ((r_pri <= eps_pri && r_dual <= eps_dual)       // solver.py:201, :373-376
+      || (prm.gap && gap_test(ctl, prm, ys, xs))) {   // solver.py:378-390
     ctl->status = GF_STATUS_SOLVED;
     ctl->iterations = k + 1;
     ctl->final_rho = rho;
@@ -685,7 +725,7 @@ static YEpi<T> make_yepi(gf_solver* s) {
   y.d = s->S->d.as<double>();
   y.yk = s->yk.as<double>(); y.yt = s->yt.as<double>(); y.cy = s->cy.as<double>();
   y.yh2 = s->yh2.as<double>(); y.nuh2 = s->nuh2.as<double>();
-  y.m = s->m; y.alpha = s->prm.alpha; y.warm_x = s->warm_x;
+  y.m = s->m; y.alpha = s->prm.alpha; y.warm_x = s->warm_x; y.gap = s->prm.gap;
   return y;
 }
 
@@ -749,7 +789,7 @@ static XEpi<T> make_xepi(gf_solver* s) {
   x.xk = s->xk.as<double>(); x.xt = s->xt.as<double>(); x.cx = s->cx.as<double>();
   x.xh2 = s->xh2.as<double>(); x.muh2 = s->muh2.as<double>();
   x.xk_T = s->xk_T.as<T>(); x.xh_T = s->xh_T.as<T>();
-  x.n = s->n; x.alpha = s->prm.alpha; x.wide = s->tall ? 0 : 1;
+  x.n = s->n; x.alpha = s->prm.alpha; x.wide = s->tall ? 0 : 1; x.gap = s->prm.gap;
   return x;
 }
 
@@ -852,7 +892,7 @@ static void launch_step_wide(gf_solver* s, int64_t k, cudaStream_t st) {
   ye.ctl = ctl; ye.f = s->f.view; ye.d = s->S->d.as<double>();
   ye.yk = s->yk.as<double>(); ye.yt = s->yt.as<double>(); ye.cy = s->cy.as<double>();
   ye.yh2 = s->yh2.as<double>(); ye.nuh2 = s->nuh2.as<double>(); ye.ypl = s->ypl.as<double>();
-  ye.rhs_T = s->rhs_T.as<T>(); ye.m = s->m; ye.alpha = s->prm.alpha;
+  ye.rhs_T = s->rhs_T.as<T>(); ye.m = s->m; ye.alpha = s->prm.alpha; ye.gap = s->prm.gap;
   s->mark(1, st, true);
   rowgemv_kernel<T, 2, YEpiW<T>><<<(unsigned)s->grid_r, kRowThreads, 0, st>>>(
       (const T*)A->data, s->m, s->ld, s->xk_T.as<T>(), s->xh_T.as<T>(), ye, s->rpart.as<double>());
@@ -944,6 +984,8 @@ static void fill_state(gf_solver* s, gf_solver_state* st) {
   st->rho = c.rho;
   st->final_rho = c.status == GF_STATUS_RUNNING ? c.rho : c.final_rho;
   st->inner_iterations = c.inner;
+  st->gap = c.gap_set ? c.gap : NAN;
+  st->gap_valid = c.gap_set ? 1 : 0;
 }
 
 }  // namespace gf
@@ -967,9 +1009,13 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
   GF_REQUIRE(f->n == s->m, GF_E_DIMENSION, "f length does not match the rows of A");
   GF_REQUIRE(g->n == s->n, GF_E_DIMENSION, "g length does not match the columns of A");
   s->prm = Params{st_in->abs_tol, st_in->rel_tol, st_in->alpha, st_in->delta, st_in->tau, st_in->max_iter,
-                  st_in->adaptive_rho};
+                  st_in->adaptive_rho, 0};
   s->f.load(f, st);
   s->g.load(g, st);
+  // gap stopping needs closed-form conjugates of every term; otherwise the
+  // reference's gap is None and never stops (problem.py:79-84)
+  if (st_in->gap_stop)
+    s->prm.gap = (conj_supported(s->f.view, s->m, st) && conj_supported(s->g.view, s->n, st)) ? 1 : 0;
   const int sms = num_sms();
   const int64_t n = s->n, m1 = std::max<int64_t>(s->m, 1), es = A->esize();
   s->grid_r = row_grid(m1, sms);

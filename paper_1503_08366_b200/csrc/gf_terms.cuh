@@ -153,6 +153,69 @@ __device__ __forceinline__ double eval_base(int kind, double x) {
   }
 }
 
+// Convex conjugate h*(w) of a base function, +inf off its domain
+// (functions.py:108-144).
+__device__ __forceinline__ double conj_base(int kind, double w) {
+  switch (kind) {
+    case kAbs: return fabs(w) <= 1.0 ? 0.0 : INFINITY;
+    case kSquare: return M_(M_(0.5, w), w);
+    case kHuber: return fabs(w) <= 1.0 ? M_(M_(0.5, w), w) : INFINITY;
+    case kNegEntr: return exp(S_(w, 1.0));
+    case kLogistic: {   // binary entropy on [0, 1]
+      if (!(w >= 0.0 && w <= 1.0)) return INFINITY;
+      const double lhs = w > 0.0 ? M_(w, log(w)) : 0.0;
+      const double rhs = w < 1.0 ? M_(S_(1.0, w), log1p(-w)) : 0.0;
+      return A_(lhs, rhs);
+    }
+    case kMaxPos0: return (w >= 0.0 && w <= 1.0) ? 0.0 : INFINITY;
+    case kIndGe0: return w <= 0.0 ? 0.0 : INFINITY;
+    case kIndLe0: return w >= 0.0 ? 0.0 : INFINITY;
+    case kIndEq0: return 0.0;
+    default: return w == 0.0 ? 0.0 : INFINITY;   // kZero
+  }
+}
+
+// Conjugate of c*h(a x - b) + d x + (e/2) x^2 at w (functions.py:329-393).
+// e == 0 reduces to h* by shift and scale; e > 0 has a closed form only for
+// Zero, Square and the three indicators -- otherwise `unsupported` is set and
+// the caller reports no gap (the reference returns None).
+__device__ __forceinline__ double conj_term(const Term& t, double w, bool& unsupported) {
+  const bool zc = t.c == 0.0;
+  const int kind = zc ? kZero : t.h;
+  const double c = zc ? 1.0 : t.c;
+  const double a = t.a, b = t.b, e = t.e;
+  const double wd = S_(w, t.d);
+  if (e == 0.0) {
+    const double q = D_(wd, M_(a, c));
+    return A_(M_(c, conj_base(kind, q)), D_(M_(b, wd), a));
+  }
+  switch (kind) {
+    case kZero: return D_(M_(wd, wd), M_(2.0, e));
+    case kSquare: {
+      const double alpha = A_(M_(M_(c, a), a), e);
+      const double beta = M_(M_(-c, a), b);
+      const double cst = M_(M_(M_(0.5, c), b), b);
+      const double tt = S_(wd, beta);
+      return S_(D_(M_(tt, tt), M_(2.0, alpha)), cst);
+    }
+    case kIndEq0:
+    case kIndGe0:
+    case kIndLe0: {
+      const double x0 = D_(b, a);
+      const double boundary = S_(M_(wd, x0), M_(M_(M_(0.5, e), x0), x0));
+      if (kind == kIndEq0) return boundary;
+      const double xbar = D_(wd, e);
+      const double interior = D_(M_(wd, wd), M_(2.0, e));
+      const bool feasible = kind == kIndGe0 ? (a > 0.0 ? xbar >= x0 : xbar <= x0)
+                                            : (a > 0.0 ? xbar <= x0 : xbar >= x0);
+      return feasible ? interior : boundary;
+    }
+    default:
+      unsupported = true;
+      return 0.0;
+  }
+}
+
 // One coordinate's contribution c*h(a v - b) + d v + e v^2 / 2; zero-weight
 // terms contribute no h part even off-domain (functions.py:321-324).
 __device__ __forceinline__ double eval_term(const Term& t, double v) {

@@ -61,6 +61,30 @@ __global__ void evaluate_final(const double* __restrict__ part, int64_t count, d
   }
 }
 
+__global__ void conj_base_kernel(int kind, int64_t n, const double* __restrict__ w, double* __restrict__ out) {
+  for (int64_t i = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = conj_base(kind, w[i]);
+}
+
+// part[block] = partial sum of conj_term; part[grid] (as bits) |= unsupported
+__global__ void conjugate_kernel(TermsView t, int64_t n, const double* __restrict__ w, double* __restrict__ part,
+                                 unsigned* __restrict__ unsup) {
+  double s = 0.0;
+  bool u = false;
+  for (int64_t i = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s += conj_term(load_term(t, i), w[i], u);
+  s = warp_sum(s);
+  if (__any_sync(0xffffffffu, u) && (threadIdx.x & 31) == 0) atomicOr(unsup, 1u);
+  __shared__ double sh[8];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int k = 0; k < 8; ++k) tot += sh[k];
+    part[blockIdx.x] = tot;
+  }
+}
+
 static unsigned egrid(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 2048)); }
 
 void prox_separable(const TermsView& t, int64_t n, const double* rho, const double* v, double* out, cudaStream_t st) {
@@ -92,6 +116,50 @@ double evaluate(const TermsView& t, int64_t n, const double* v, cudaStream_t st)
   GF_CUDA(cudaMemcpyAsync(&r, part.as<double>() + g, sizeof(double), cudaMemcpyDeviceToHost, st));
   GF_CUDA(cudaStreamSynchronize(st));
   return r;
+}
+
+__global__ void conj_support_kernel(TermsView t, int64_t n, unsigned* __restrict__ unsup) {
+  for (int64_t i = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool u = false;
+    (void)conj_term(load_term(t, i), 0.0, u);
+    if (u) atomicOr(unsup, 1u);
+  }
+}
+
+bool conj_supported(const TermsView& t, int64_t n, cudaStream_t st) {
+  if (n <= 0) return true;
+  DBuf flag(sizeof(unsigned));
+  GF_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(unsigned), st));
+  conj_support_kernel<<<egrid(n), 256, 0, st>>>(t, n, flag.as<unsigned>());
+  GF_CHECK_LAUNCH();
+  unsigned u = 0;
+  GF_CUDA(cudaMemcpyAsync(&u, flag.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  GF_CUDA(cudaStreamSynchronize(st));
+  return u == 0;
+}
+
+void conj_base(int kind, int64_t n, const double* w, double* out, cudaStream_t st) {
+  if (n <= 0) return;
+  conj_base_kernel<<<egrid(n), 256, 0, st>>>(kind, n, w, out);
+  GF_CHECK_LAUNCH();
+}
+
+double conjugate(const TermsView& t, int64_t n, const double* w, bool* supported, cudaStream_t st) {
+  *supported = true;
+  if (n <= 0) return 0.0;
+  const unsigned g = egrid(n);
+  DBuf part((g + 2) * sizeof(double));
+  GF_CUDA(cudaMemsetAsync(part.as<double>() + g + 1, 0, sizeof(double), st));
+  conjugate_kernel<<<g, 256, 0, st>>>(t, n, w, part.as<double>(), (unsigned*)(part.as<double>() + g + 1));
+  evaluate_final<<<1, 32, 0, st>>>(part.as<double>(), g, part.as<double>() + g);
+  GF_CHECK_LAUNCH();
+  double r[2] = {0.0, 0.0};
+  GF_CUDA(cudaMemcpyAsync(r, part.as<double>() + g, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  GF_CUDA(cudaStreamSynchronize(st));
+  unsigned u = 0;
+  memcpy(&u, &r[1], sizeof(u));
+  *supported = u == 0;
+  return r[0];
 }
 
 }  // namespace gf

@@ -8,9 +8,10 @@ and ``torch.distributed`` broadcasts) and issues
 
   setup      one all-reduce per Sinkhorn sweep (n column sums + scalars),
              one for the Frobenius rescale, one of the Gram matrix;
-  iteration  ONE all-reduce of 2*ld + 6 doubles between the column pass and
+  iteration  ONE all-reduce of 2*ld + 8 doubles between the column pass and
              the controller: [A_hat' c_y | A_hat' nu^ | r_pri^2, ||y||^2,
-             f(y), drift, flags]; every rank then takes the same decision.
+             f(y), drift, flags, and the two gap terms]; every rank then
+             takes the same decision.
 
 Usage (under torchrun, after ``torch.distributed.init_process_group``)::
 

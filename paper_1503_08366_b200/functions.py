@@ -184,10 +184,11 @@ class SeparableFunction:
         return _native.evaluate(self, v)
 
     def conjugate(self, w):
-        """Coordinatewise conjugate sum (functions.py:329-365); the gap-based
-        stopping rule that needs it is a later-round item."""
-        raise NotImplementedError(
-            "conjugates / gap-based stopping are not in this build yet")
+        """Coordinatewise conjugate sum, or ``None`` when some term has e > 0
+        and a kind whose composition has no closed form (functions.py:329-393).
+        Runs on the GPU."""
+        from . import _native
+        return _native.conjugate(self, w)
 
 
 def eval_base(h, x):
@@ -197,4 +198,7 @@ def eval_base(h, x):
 
 
 def conjugate_base(h, w):
-    raise NotImplementedError("conjugates are not in this build yet")
+    """Convex conjugate of base function ``h`` elementwise (functions.py:147-150),
+    on the GPU."""
+    from . import _native
+    return _native.conj_base(kind_code(h), w)

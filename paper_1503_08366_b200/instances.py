@@ -21,7 +21,7 @@ from .errors import ParameterError
 from .functions import BaseFunction, SeparableFunction
 from .problem import GraphFormProblem
 
-__all__ = ["FAMILIES", "GenSpec", "generate", "tall_lasso", "canonical_family"]
+__all__ = ["FAMILIES", "GenSpec", "generate", "tall_lasso", "tall_ridge", "canonical_family"]
 
 # Family order fixes the SeedSequence index (generators.py:25-35).
 FAMILIES = (
@@ -103,6 +103,14 @@ def tall_lasso(m: int, n: int, seed: int = 0, dtype=np.float64):
     f = SeparableFunction.from_arrays(BaseFunction.SQUARE, size=m, b=b)
     g = SeparableFunction.from_arrays(BaseFunction.ABS, size=n, c=lam)
     return GraphFormProblem(A, f, g), {"v": v, "b": b, "lam": lam}
+
+
+def tall_ridge(m: int, n: int, seed: int = 0, dtype=np.float64):
+    """tall_lasso's data with g = lam * Square (every conjugate finite: the
+    duality gap is a usable stopping rule; test fixture family)."""
+    problem, meta = tall_lasso(m, n, seed, dtype)
+    g = SeparableFunction.from_arrays(BaseFunction.SQUARE, size=n, c=meta["lam"])
+    return GraphFormProblem(problem.A, problem.f, g), meta
 
 
 def _gen_lasso(s):

@@ -28,7 +28,7 @@ import numpy as np
 from . import _native
 from .equilibration import Equilibration
 from .errors import DimensionError, ParameterError
-from .problem import GraphFormProblem
+from .problem import GraphFormProblem, duality_gap
 from .projection import ProjectorCache, _dtype_for
 
 __all__ = ["Status", "SolverSettings", "SolveResult", "Setup", "IterationSnapshot", "prepare",
@@ -210,7 +210,8 @@ def _gf_settings(s: SolverSettings):
         rho0=float(s.rho0), abs_tol=float(s.abs_tol), rel_tol=float(s.rel_tol),
         max_iter=int(s.max_iter), alpha=float(s.alpha), adaptive_rho=1 if s.adaptive_rho else 0,
         delta=float(s.delta), tau=float(s.tau), projection=0 if s.projection == "direct" else 1,
-        projection_tol=float(s.projection_tol) if s.projection_tol is not None else -1.0)
+        projection_tol=float(s.projection_tol) if s.projection_tol is not None else -1.0,
+        gap_stop=1 if s.gap_stop else 0)
 
 
 _VERBOSE_HEADER = (f"{'iter':>6} {'r_pri':>11} {'eps_pri':>11} {'r_dual':>11} "
@@ -287,8 +288,6 @@ def solve(problem: GraphFormProblem, settings: SolverSettings = None, *,
     rank's rows of a row-partitioned problem (see ``distributed.py``)."""
     if settings is None:
         settings = SolverSettings()
-    if settings.gap_stop:
-        raise NotImplementedError("gap-based stopping is not in this build (SURVEY §8f)")
     own = setup is None
     if own:
         setup = prepare(problem, settings, scaling=scaling, comm=comm)
@@ -329,7 +328,8 @@ def solve(problem: GraphFormProblem, settings: SolverSettings = None, *,
     x, y, mu, nu, st = run.result()
     return SolveResult(
         x=x, y=y, mu=mu, nu=nu, objective=float(st.objective),
-        primal_residual=float(st.r_pri), dual_residual=float(st.r_dual), gap=None,
+        primal_residual=float(st.r_pri), dual_residual=float(st.r_dual),
+        gap=float(st.gap) if st.gap_valid else None,
         status=_STATUS[st.status], iterations=int(st.iterations),
         solve_time=time.perf_counter() - t0, setup_time=setup_time, final_rho=float(st.final_rho))
 
@@ -375,7 +375,17 @@ def residual_stop(A, x_half, y_half, mu_half, nu_half, eps_abs, eps_rel):
 
 
 def gap_stop(problem, x_full, y_full, mu_full, nu_full, eps_abs, eps_rel):
-    raise NotImplementedError("gap-based stopping is not in this build (SURVEY §8f)")
+    """Gap-based stopping test at the full iterate (solver.py:205-218):
+    ``(stop, gap)``; ``gap`` is None when a conjugate is unsupported and an
+    infinite gap never stops.  The solve runs this test inside its device
+    controller; this is the standalone form (conjugates on the GPU)."""
+    gap = duality_gap(problem, x_full, y_full, mu_full, nu_full)
+    if gap is None or not np.isfinite(gap):
+        return False, gap
+    obj = problem.objective(x_full, y_full)
+    if not np.isfinite(obj):
+        return False, gap
+    return gap <= eps_abs + eps_rel * abs(obj), gap
 
 
 def adapt_rho(rho, xt, yt, k, l, u, r_pri, r_dual, eps_pri, eps_dual, delta, tau):

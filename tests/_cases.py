@@ -42,8 +42,9 @@ def build_problem(fx, as_float32=False):
     m, n, seed = int(m), int(n), int(seed)
     r32 = kind.endswith("32")
     base = kind[:-2] if r32 else kind
-    if base == "tall_lasso":
-        problem, _ = instances.tall_lasso(m, n, seed, dtype=np.float32 if r32 else np.float64)
+    if base in ("tall_lasso", "tall_ridge"):
+        build = instances.tall_lasso if base == "tall_lasso" else instances.tall_ridge
+        problem, _ = build(m, n, seed, dtype=np.float32 if r32 else np.float64)
         A = np.asarray(problem.A, np.float64)
     else:
         problem, _ = instances.generate(instances.GenSpec(base, m, n, seed))

@@ -130,7 +130,51 @@ def make_projection():
     save("projection", **out)
 
 
+# ---------------------------------------------------------- conjugates ----
+def make_conj():
+    rng = np.random.default_rng(1503)
+    out = {}
+    n = 2000
+    for code, kind in enumerate(gf.BaseFunction):
+        w = rng.uniform(-3, 3, n)
+        w[:8] = [0.0, 1.0, -1.0, 0.5, 1e-300, 1.0 - 1e-16, 2.0, -0.0]
+        out[f"k{code}_w"] = w
+        out[f"k{code}_base"] = gf.conjugate_base(kind, w)
+        # separable terms of this kind: e == 0 (shift/scale rules) and, for
+        # every kind, a second set with e > 0 (closed form or None)
+        for tag, epos in (("e0", False), ("ep", True)):
+            a = rng.uniform(0.3, 3.0, n) * rng.choice([-1.0, 1.0], n)
+            b = rng.normal(0, 1, n)
+            c = rng.uniform(0.1, 3.0, n)
+            c[rng.random(n) < 0.1] = 0.0
+            d = rng.normal(0, 1, n)
+            e = rng.uniform(0.2, 2.0, n) if epos else np.zeros(n)
+            sf = gf.SeparableFunction.from_arrays(kind, size=n, a=a, b=b, c=c, d=d, e=e)
+            ww = rng.uniform(-2, 2, n)
+            val = sf.conjugate(ww)
+            for k2, arr in dict(a=a, b=b, c=c, d=d, e=e, w=ww).items():
+                out[f"k{code}_{tag}_{k2}"] = arr
+            out[f"k{code}_{tag}_val"] = np.array(np.nan if val is None else val)
+            out[f"k{code}_{tag}_none"] = np.array(val is None)
+    # duality gap of a solved ridge problem at its full iterate
+    problem = tall_ridge(300, 60, 4)
+    r = gf.solve(problem, gf.SolverSettings(abs_tol=1e-8, rel_tol=1e-8))
+    out["gap_x"], out["gap_y"], out["gap_mu"], out["gap_nu"] = r.x, r.y, r.mu, r.nu
+    out["gap_val"] = np.array(gf.duality_gap(problem, r.x, r.y, r.mu, r.nu))
+    out["gap_sha"] = np.array(sha(problem.A))
+    save("conj", **out)
+
+
 # ---------------------------------------------------------------- solve ----
+def tall_ridge(m, n, seed):
+    """tall_lasso's data with g = lam * Square: every conjugate is finite, so
+    the duality gap is a usable stopping rule."""
+    p = tall_lasso(m, n, seed)
+    lam = float(p.g.c[0])
+    g = gf.SeparableFunction.from_arrays(gf.BaseFunction.SQUARE, size=n, c=lam)
+    return gf.GraphFormProblem(p.A, p.f, g)
+
+
 def tall_lasso(m, n, seed, fp32=False):
     root = np.random.SeedSequence([seed, 3])
     ra, rv, rn = (np.random.default_rng(s) for s in root.spawn(3))
@@ -183,6 +227,13 @@ SOLVE_CASES = [
     ("lasso_tall_1000x200_alpha", ("tall_lasso", 1000, 200, 0), {"alpha": 1.0, "abs_tol": 1e-5, "rel_tol": 1e-4}, {}),
     ("lasso_tall_1000x200_indirect", ("tall_lasso", 1000, 200, 0), {"projection": "indirect"}, {}),
     ("svm_2000x100_warm", ("svm", 2000, 100, 3), {}, {"warm": True}),
+    # gap-based stopping (solver.py:378-390): finite gap (ridge), a gap that
+    # is infinite on most iterations (Lasso: |mu| <= lam), an indicator g
+    ("ridge_tall_600x150_gap", ("tall_ridge", 600, 150, 0), {"gap_stop": True}, {}),
+    ("ridge_tall_600x150_gap_loose", ("tall_ridge", 600, 150, 1),
+     {"gap_stop": True, "abs_tol": 1e-3, "rel_tol": 1e-2}, {}),
+    ("lasso_tall_1000x200_gap", ("tall_lasso", 1000, 200, 0), {"gap_stop": True}, {}),
+    ("nnls_600x150_gap", ("nnls", 600, 150, 0), {"gap_stop": True}, {}),
 ]
 
 
@@ -192,6 +243,8 @@ def build(desc):
         return tall_lasso(m, n, seed)
     if kind == "tall_lasso32":
         return tall_lasso(m, n, seed, fp32=True)
+    if kind == "tall_ridge":
+        return tall_ridge(m, n, seed)
     if kind.endswith("32"):
         return round32(gf.generate(gf.GenSpec(kind[:-2], m, n, seed))[0])
     return gf.generate(gf.GenSpec(kind, m, n, seed))[0]
@@ -221,6 +274,7 @@ def make_solves(only=None):
             sha_A=np.array(sha(problem.A)), desc=np.array([str(x) for x in desc]),
             settings=np.array(repr(skw)), d=setup.scaling.d, e=setup.scaling.e,
             eq_iters=np.array(setup.scaling.iterations),
+            gap=np.array(np.nan if r.gap is None else r.gap), gap_none=np.array(r.gap is None),
         )
         arrays.update({f"f_{k}": getattr(problem.f, k) for k in "habcde"})
         arrays.update({f"g_{k}": getattr(problem.g, k) for k in "habcde"})
@@ -238,4 +292,6 @@ if __name__ == "__main__":
         make_prox()
         make_equil()
         make_projection()
+    if not only or "conj" in only:
+        make_conj()
     make_solves(only)

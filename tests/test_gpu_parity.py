@@ -15,6 +15,7 @@ import pytest
 import paper_1503_08366_b200 as gf
 from oracle import graphform_oracle as orc
 from tests import _cases
+from tests.test_oracle_golden import check_gap
 
 pytestmark = pytest.mark.gpu
 
@@ -166,6 +167,10 @@ def test_solve_fp64_matches_reference(name):
         assert close(getattr(res, k), fx[k], 1e-5), k
     assert abs(res.objective - float(fx["objective"])) <= 1e-5 * max(1.0, abs(float(fx["objective"])))
     assert res.final_rho == pytest.approx(float(fx["final_rho"]), rel=1e-9)
+    if _cases.settings_of(fx).get("gap_stop"):
+        check_gap(res.gap, fx, rtol=1e-6)
+    else:
+        assert res.gap is None
 
 
 @pytest.mark.parametrize("name", CHAOTIC)
@@ -266,3 +271,47 @@ def test_gram_tensor_core_fp32(shape):
     # 512 rows: measured ~5e-6 (tools/syrk_accuracy.py); plain TF32 gives ~4e-4
     assert err < 1.5e-5, err
     np.testing.assert_allclose(G, G.T, rtol=0, atol=0)
+
+
+CONJ = _cases.load("conj")
+
+
+@pytest.mark.parametrize("code", range(10))
+def test_conjugates_match_reference(code):
+    """conjugate_base and SeparableFunction.conjugate (functions.py:108-393) on
+    the GPU against the reference's values (None = unsupported e > 0 kind)."""
+    kind = list(gf.BaseFunction)[code]
+    w = CONJ[f"k{code}_w"]
+    z = gf.conjugate_base(kind, w)
+    ref = CONJ[f"k{code}_base"]
+    np.testing.assert_array_equal(np.isinf(z), np.isinf(ref))
+    fin = np.isfinite(ref)
+    np.testing.assert_allclose(z[fin], ref[fin], rtol=1e-13, atol=1e-300)
+    for tag in ("e0", "ep"):
+        p = {k: CONJ[f"k{code}_{tag}_{k}"] for k in "abcdew"}
+        sf = gf.SeparableFunction.from_arrays(kind, size=len(p["w"]), a=p["a"], b=p["b"], c=p["c"],
+                                              d=p["d"], e=p["e"])
+        val = sf.conjugate(p["w"])
+        if bool(CONJ[f"k{code}_{tag}_none"]):
+            assert val is None
+        else:
+            r = float(CONJ[f"k{code}_{tag}_val"])
+            assert val == r or abs(val - r) <= 1e-10 * max(1.0, abs(r)), (val, r)
+
+
+def test_duality_gap_and_gap_stop_helpers():
+    from paper_1503_08366_b200 import instances
+    prob, _ = instances.tall_ridge(300, 60, 4)
+    g = gf.duality_gap(prob, CONJ["gap_x"], CONJ["gap_y"], CONJ["gap_mu"], CONJ["gap_nu"])
+    assert abs(g - float(CONJ["gap_val"])) <= 1e-9
+    stop, g2 = gf.gap_stop(prob, CONJ["gap_x"], CONJ["gap_y"], CONJ["gap_mu"], CONJ["gap_nu"], 1e-4, 1e-3)
+    assert stop and g2 == g
+    # SPEC.md:350 -- f = g = Zero, all state zero: gap 0, stop
+    z = gf.SeparableFunction.from_arrays("zero", size=3)
+    p0 = gf.GraphFormProblem(np.ones((3, 3)), z, z)
+    assert gf.gap_stop(p0, np.zeros(3), np.zeros(3), np.zeros(3), np.zeros(3), 1e-4, 1e-3) == (True, 0.0)
+    # an unsupported conjugate (e > 0 with Abs) gives None and never stops
+    ab = gf.SeparableFunction.from_arrays("abs", size=3, e=1.0)
+    p1 = gf.GraphFormProblem(np.ones((3, 3)), ab, z)
+    assert gf.duality_gap(p1, np.zeros(3), np.zeros(3), np.zeros(3), np.zeros(3)) is None
+    assert gf.gap_stop(p1, np.zeros(3), np.zeros(3), np.zeros(3), np.zeros(3), 1e-4, 1e-3) == (False, None)

@@ -106,3 +106,48 @@ def test_oracle_solve_matches_reference(name):
         assert close(res[k], fx[k], 1e-9), k
     assert abs(res["objective"] - float(fx["objective"])) <= 1e-9 * max(1, abs(float(fx["objective"])))
     assert abs(res["final_rho"] - float(fx["final_rho"])) <= 1e-12 * float(fx["final_rho"])
+    if "gap" in fx and _cases.settings_of(fx).get("gap_stop"):
+        check_gap(res["gap"], fx)
+
+
+def check_gap(gap, fx, rtol=1e-8):
+    """SolveResult.gap against the reference: None, inf, or a finite value."""
+    if bool(fx["gap_none"]):
+        assert gap is None
+    elif np.isinf(fx["gap"]):
+        assert gap is not None and np.isinf(gap)
+    else:
+        ref = float(fx["gap"])
+        assert gap is not None and abs(gap - ref) <= rtol * max(1.0, abs(ref)), (gap, ref)
+
+
+CONJ = _cases.load("conj")
+
+
+@pytest.mark.parametrize("code", range(10))
+def test_oracle_conjugates_match_reference(code):
+    w = CONJ[f"k{code}_w"]
+    z = orc.conj_kind(code, w)
+    ref = CONJ[f"k{code}_base"]
+    np.testing.assert_array_equal(np.isinf(z), np.isinf(ref))
+    fin = np.isfinite(ref)
+    np.testing.assert_allclose(z[fin], ref[fin], rtol=1e-14, atol=1e-300)
+    for tag in ("e0", "ep"):
+        p = {k: CONJ[f"k{code}_{tag}_{k}"] for k in "abcdew"}
+        t = orc.Terms.make(code, len(p["w"]), p["a"], p["b"], p["c"], p["d"], p["e"])
+        val = orc.conjugate(t, p["w"])
+        if bool(CONJ[f"k{code}_{tag}_none"]):
+            assert val is None
+        else:
+            ref = float(CONJ[f"k{code}_{tag}_val"])
+            assert val == ref or abs(val - ref) <= 1e-11 * max(1.0, abs(ref)), (val, ref)
+
+
+def test_oracle_duality_gap_at_solution():
+    from paper_1503_08366_b200 import instances
+    prob, _ = instances.tall_ridge(300, 60, 4)
+    import hashlib
+    assert hashlib.sha256(np.ascontiguousarray(prob.A).tobytes()).hexdigest() == str(CONJ["gap_sha"])
+    g = orc.duality_gap(orc.Terms.of(prob.f), orc.Terms.of(prob.g), CONJ["gap_x"], CONJ["gap_y"],
+                        CONJ["gap_mu"], CONJ["gap_nu"])
+    assert abs(g - float(CONJ["gap_val"])) <= 1e-9
