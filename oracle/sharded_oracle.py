@@ -12,7 +12,8 @@ payloads the device issues:
   projector        I + sum_r A_r' A_r           (n x n, once)
   iteration        [ A_hat' c_y (n) | A' nu_half (n) |
                      ||A x_half - y_half||^2, ||y_half||^2, f(y_half),
-                     ||y_half_hat - y_hat||^2 ]  (one all-reduce)
+                     ||y_half_hat - y_hat||^2, f(y_full), f*(nu_full) ]
+                   (one all-reduce; the last two only with gap_stop)
   indirect CGLS    A_hat' r and the m-length dot products
 
 so a world-size-2 ``gloo`` run on CPU checks that the decomposition
@@ -127,10 +128,14 @@ def solve(A_loc, f_loc: orc.Terms, g: orc.Terms, m_glob, allreduce, settings=Non
         rx = alpha * xhh + (1.0 - alpha) * xk
         ry = alpha * yhh + (1.0 - alpha) * yk
         cx, cy = rx + xt, ry + yt
+        gy = [0.0, 0.0]
+        if s["gap_stop"]:   # full iterate of this rank's rows (solver.py:379-382)
+            fc = orc.conjugate(f_loc, -rho * d * yt)
+            gy = [orc.evaluate(f_loc, yk / d), np.nan if fc is None else fc]
         red = allreduce(np.concatenate([
             Ah.T @ cy, A_loc.T @ nuh,
             [float(np.sum((A_loc @ xh - yh) ** 2)), float(yh @ yh), orc.evaluate(f_loc, yh),
-             float(np.sum((yhh - yk) ** 2))]]))
+             float(np.sum((yhh - yk) ** 2))], gy]))
         aty, atnu = red[:n], red[n:2 * n]
         r_pri = float(np.sqrt(red[2 * n]))
         r_dual = float(np.linalg.norm(atnu + muh))
@@ -141,6 +146,16 @@ def solve(A_loc, f_loc: orc.Terms, g: orc.Terms, m_glob, allreduce, settings=Non
         if r_pri <= eps_pri and r_dual <= eps_dual:
             status, iters = "Solved", k + 1
             break
+        if s["gap_stop"]:
+            gc = orc.conjugate(g, -rho * xt / e)
+            fyf, fcj = red[2 * n + 4], red[2 * n + 5]
+            if gc is not None and not np.isnan(fcj):
+                gxf = orc.evaluate(g, e * xk)
+                gap = fyf + fcj + gxf + gc
+                objf = fyf + gxf
+                if np.isfinite(gap) and np.isfinite(objf) and gap <= s["abs_tol"] + s["rel_tol"] * abs(objf):
+                    status, iters = "Solved", k + 1
+                    break
         if indirect:
             if s["projection_tol"] is not None:
                 ptol = s["projection_tol"]

@@ -25,7 +25,8 @@ from tests import _cases
 
 CASES = ["lasso_tall_1000x200", "lasso_tall_1000x200_alpha", "lasso_tall_1000x200_fixedrho",
          "lasso_tall_1000x200_indirect", "lasso_tall_1000x200_maxit", "lasso_tall_1000x200_noeq",
-         "huber_fit_400x80", "nnls_600x150", "svm_2000x100", "lp_600x240", "basis_pursuit_500x120"]
+         "huber_fit_400x80", "nnls_600x150", "svm_2000x100", "lp_600x240", "basis_pursuit_500x120",
+         "ridge_tall_600x150_gap", "nnls_600x150_gap"]
 # Not here: the logistic cases.  The reference's safeguarded Newton
 # (prox.py:27-48) exits unconverged after 100 steps for some coordinates
 # (e.g. rho_h = 0.031, z0 = 29: Newton oscillates across the root until the
