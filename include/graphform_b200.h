@@ -218,6 +218,26 @@ int gf_solver_elapsed_ms(gf_solver* s, double* ms);
 int gf_solver_stats(gf_solver* s, int64_t* launches, double* kernel_ms, int64_t* kernel_count);
 int gf_solver_profile(gf_solver* s, int enable);
 
+/* ------------------------------------------- input synthesis (§8f item 1) -- */
+/* numpy Generator(PCG64).normal(loc, scale, size=count) -- the streams of the
+ * reference generators (generators.py:80-264) -- bit for bit on the device.
+ * (state, inc) is the generator's bit_generator.state (128-bit halves).
+ * Normal j is written to out[(j / ncol) * rs + (j % ncol) * cs] as dtype
+ * (GF_F32 rounds the fp64 value).  out is DEVICE memory. */
+int gf_normal_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
+                   double loc, double scale, int dtype, void* out, int64_t ncol, int64_t rs, int64_t cs,
+                   void* stream);
+/* y = A x / y = A' x over a raw DEVICE matrix (m x n, row stride lda elements,
+ * 16-byte aligned rows), fp64 accumulation; x, y DEVICE fp64.  The generators'
+ * A @ v and A.T @ b. */
+int gf_dense_matvec(int dtype, int64_t m, int64_t n, const void* A, int64_t lda, int transpose,
+                    const double* x, double* y, void* stream);
+/* A_ij <- s_i * (A_ij + t_i) on a DEVICE fp64 matrix (svm generator). */
+int gf_rows_affine(int64_t m, int64_t n, double* A, int64_t lda, const double* s, const double* t, void* stream);
+/* dst (dtype, row stride ldd) <- src (fp64, row stride lds), DEVICE. */
+int gf_convert_matrix(int64_t m, int64_t n, const double* src, int64_t lds, int dtype, void* dst, int64_t ldd,
+                      void* stream);
+
 /* ----------------------------------------------- multi-GPU (row shards) -- */
 /* NCCL communicator for one process per GPU; the 128-byte unique id is made
  * by rank 0 and broadcast by the caller (torch.distributed in the host). */

@@ -97,6 +97,11 @@ _SIGS = {
     "gf_solver_elapsed_ms": ([_P, c_double_p], C.c_int),
     "gf_solver_stats": ([_P, c_int64_p, _P, _P], C.c_int),
     "gf_solver_profile": ([_P, C.c_int], C.c_int),
+    "gf_normal_fill": ([C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.c_double, C.c_double,
+                        C.c_int, _P, C.c_int64, C.c_int64, C.c_int64, _P], C.c_int),
+    "gf_dense_matvec": ([C.c_int, C.c_int64, C.c_int64, _P, C.c_int64, C.c_int, _P, _P, _P], C.c_int),
+    "gf_rows_affine": ([C.c_int64, C.c_int64, _P, C.c_int64, _P, _P, _P], C.c_int),
+    "gf_convert_matrix": ([C.c_int64, C.c_int64, _P, C.c_int64, C.c_int, _P, C.c_int64, _P], C.c_int),
     "gf_comm_unique_id": ([C.c_char_p], C.c_int),
     "gf_comm_create": ([C.c_char_p, C.c_int, C.c_int, C.POINTER(_P)], C.c_int),
     "gf_comm_destroy": ([_P], C.c_int),
@@ -291,15 +296,69 @@ def eval_base(code, x):
     return like_input(out, x)
 
 
+# ----------------------------------------------------- input synthesis --
+_M64 = (1 << 64) - 1
+
+
+def normal_fill(rng, out, count, loc=0.0, scale=1.0, ncol=None, rs=None, cs=1):
+    """Write ``rng.normal(loc, scale, size=count)`` (numpy Generator on PCG64)
+    into the CUDA tensor ``out``: normal j lands at flat offset
+    (j // ncol) * rs + (j % ncol) * cs.  Bit-identical to numpy."""
+    import torch
+    st = rng.bit_generator.state
+    if st.get("bit_generator") != "PCG64":
+        raise ParameterError("device sampling reproduces PCG64 streams only")
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    dt = GF_F32 if out.dtype == torch.float32 else GF_F64
+    ncol = int(count) if ncol is None else int(ncol)
+    rs = ncol if rs is None else int(rs)
+    check(lib().gf_normal_fill(s >> 64, s & _M64, inc >> 64, inc & _M64, int(count), float(loc), float(scale),
+                               dt, ptr(out), ncol, int(rs), int(cs), stream()))
+
+
+def dense_matvec(A, x, transpose=False):
+    """fp64 A @ x (or A.T @ x) over a CUDA matrix with unit column stride."""
+    import torch
+    L = lib()
+    if A.stride(1) != 1:
+        raise ParameterError("matrix must have unit column stride")
+    m, n = int(A.shape[0]), int(A.shape[1])
+    x_t = to_device64(x)
+    y = torch.empty(n if transpose else m, dtype=torch.float64, device=A.device)
+    dt = GF_F32 if A.dtype == torch.float32 else GF_F64
+    check(L.gf_dense_matvec(dt, m, n, ptr(A), int(A.stride(0)), 1 if transpose else 0, ptr(x_t), ptr(y), stream()))
+    return y
+
+
+def rows_affine(A, s, t):
+    """A_ij <- s_i * (A_ij + t_i) in place (fp64 CUDA matrix)."""
+    s_t, t_t = to_device64(s), to_device64(t)
+    check(lib().gf_rows_affine(int(A.shape[0]), int(A.shape[1]), ptr(A), int(A.stride(0)), ptr(s_t), ptr(t_t),
+                               stream()))
+
+
+def convert_matrix(src, dst):
+    """dst <- src (fp64 -> dst's dtype), both CUDA, unit column stride."""
+    import torch
+    dt = GF_F32 if dst.dtype == torch.float32 else GF_F64
+    check(lib().gf_convert_matrix(int(src.shape[0]), int(src.shape[1]), ptr(src), int(src.stride(0)), dt, ptr(dst),
+                                  int(dst.stride(0)), stream()))
+
+
 class Matrix:
     """Owning handle of a gf_matrix (library-side padded copy of A)."""
 
     def __init__(self, A, dtype: int):
         L = lib()
         self._lib = L
+        src_ld = None
         if is_torch(A):
             import torch
-            src = A.contiguous()
+            src = A
+            if src.is_cuda and src.dim() == 2 and src.stride(1) == 1 and src.dtype in (torch.float32, torch.float64):
+                src_ld = int(src.stride(0))    # row-strided device view (e.g. a padded buffer): no copy
+            else:
+                src = src.contiguous()
             if src.dtype not in (torch.float32, torch.float64):
                 src = src.to(torch.float64)
             if not src.is_cuda:
@@ -312,7 +371,7 @@ class Matrix:
         sdt = GF_F32 if str(src.dtype).endswith("float32") else GF_F64
         h = C.c_void_p()
         check(L.gf_matrix_create(dtype, self.m, self.n, ptr(src) if self.m else None, sdt,
-                                 self.n, stream(), C.byref(h)))
+                                 src_ld if src_ld is not None else self.n, stream(), C.byref(h)))
         self.handle = h
         self.dtype = dtype
         self.owned = True

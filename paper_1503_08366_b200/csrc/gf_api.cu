@@ -273,6 +273,52 @@ int gf_eval_base(int64_t n, int kind, const double* x, double* out, void* stream
   });
 }
 
+int gf_normal_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
+                   double loc, double scale, int dtype, void* out, int64_t ncol, int64_t rs, int64_t cs,
+                   void* stream) {
+  return guarded([&] {
+    GF_REQUIRE(dtype == GF_F32 || dtype == GF_F64, GF_E_PARAMETER, "dtype must be GF_F32 or GF_F64");
+    GF_REQUIRE(count >= 0 && ncol >= 1, GF_E_DIMENSION, "count must be >= 0 and ncol >= 1");
+    normal_fill(state_hi, state_lo, inc_hi, inc_lo, count, loc, scale, dtype, out, ncol, rs, cs,
+                (cudaStream_t)stream);
+  });
+}
+
+int gf_dense_matvec(int dtype, int64_t m, int64_t n, const void* A, int64_t lda, int transpose, const double* x,
+                    double* y, void* stream) {
+  return guarded([&] {
+    GF_REQUIRE(dtype == GF_F32 || dtype == GF_F64, GF_E_PARAMETER, "dtype must be GF_F32 or GF_F64");
+    const int64_t es = dtype == GF_F32 ? 4 : 8;
+    GF_REQUIRE(m >= 0 && n >= 0 && lda >= n, GF_E_DIMENSION, "bad matrix shape / row stride");
+    GF_REQUIRE(((uintptr_t)A % 16) == 0 && (lda * es) % 16 == 0, GF_E_PARAMETER,
+               "matrix rows must be 16-byte aligned");
+    gf_matrix view;
+    view.dtype = dtype; view.m = m; view.n = n; view.ld = lda; view.data = const_cast<void*>(A);
+    if (m == 0 || n == 0) {
+      GF_CUDA(cudaMemsetAsync(y, 0, (transpose ? n : m) * sizeof(double), (cudaStream_t)stream));
+      GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+      return;
+    }
+    matvec(&view, transpose != 0, x, y, (cudaStream_t)stream);
+  });
+}
+
+int gf_rows_affine(int64_t m, int64_t n, double* A, int64_t lda, const double* s, const double* t, void* stream) {
+  return guarded([&] {
+    rows_affine(m, n, A, lda, s, t, (cudaStream_t)stream);
+    GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  });
+}
+
+int gf_convert_matrix(int64_t m, int64_t n, const double* src, int64_t lds, int dtype, void* dst, int64_t ldd,
+                      void* stream) {
+  return guarded([&] {
+    GF_REQUIRE(dtype == GF_F32 || dtype == GF_F64, GF_E_PARAMETER, "dtype must be GF_F32 or GF_F64");
+    store_matrix(src, lds, dtype, dst, ldd, m, n, (cudaStream_t)stream);
+    GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  });
+}
+
 int gf_conj_base(int64_t n, int kind, const double* w, double* out, void* stream) {
   return guarded([&] {
     GF_REQUIRE(kind >= 0 && kind <= 9, GF_E_PARAMETER, "unknown base function code");

@@ -107,6 +107,12 @@ int64_t project_indirect_dev(const gf_matrix* A, bool tall, gf_comm* comm, const
                              const double* xw, const double* yw, double tol, int64_t max_inner, double* x,
                              double* y, bool* ok, cudaStream_t st);
 
+// ------------------------------------------------- input synthesis (gf_rng) --
+void normal_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
+                 double loc, double scale, int dtype, void* out, int64_t ncol, int64_t rs, int64_t cs,
+                 cudaStream_t st);
+void rows_affine(int64_t m, int64_t n, double* A, int64_t lda, const double* s, const double* t, cudaStream_t st);
+
 // ------------------------------------------------------------- NCCL glue --
 void allreduce_sum(gf_comm* c, double* buf, size_t count, cudaStream_t st);
 
