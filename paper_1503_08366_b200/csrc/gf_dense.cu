@@ -312,15 +312,15 @@ void inverse_from_factor_inv(const double* W, int64_t q, int64_t ld, double* Gin
 template <typename T>
 __global__ void convert_pad(const double* __restrict__ src, int64_t lds, T* __restrict__ dst,
                             int64_t ldd, int64_t rows, int64_t cols) {
-  const int64_t i = blockIdx.y;
-  for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < ldd; j += (int64_t)gridDim.x * blockDim.x)
-    dst[i * ldd + j] = j < cols ? (T)src[i * lds + j] : (T)0;
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y)
+    for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < ldd; j += (int64_t)gridDim.x * blockDim.x)
+      dst[i * ldd + j] = j < cols ? (T)src[i * lds + j] : (T)0;
 }
 
 void store_matrix(const double* src, int64_t lds, int dtype, void* dst, int64_t ldd, int64_t rows,
                   int64_t cols, cudaStream_t st) {
   if (rows <= 0) return;
-  dim3 grid((unsigned)std::min<int64_t>(ceil_div(ldd, 256), 64), (unsigned)rows);
+  dim3 grid((unsigned)std::min<int64_t>(ceil_div(ldd, 256), 64), (unsigned)std::min<int64_t>(rows, 65535));
   if (dtype == GF_F32) convert_pad<float><<<grid, 256, 0, st>>>(src, lds, (float*)dst, ldd, rows, cols);
   else convert_pad<double><<<grid, 256, 0, st>>>(src, lds, (double*)dst, ldd, rows, cols);
   GF_CHECK_LAUNCH();
