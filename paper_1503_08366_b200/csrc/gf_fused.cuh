@@ -41,8 +41,11 @@ constexpr int kMaxSlots = 32;
 // while the latency from R(ge) to its weights stays under the two-period lag.
 // Three: 16 + 3 + 1 = 20 warps keeps 5 warps per SM sub-partition (96 registers
 // per thread); with 20 compute warps the CTA has 24 warps (80 registers).
-constexpr int kFusedEpiMax = 3;
-__host__ __device__ constexpr int fused_epi(int cw) { return 3; }
+#ifndef GF_FUSED_NE
+#define GF_FUSED_NE 3
+#endif
+constexpr int kFusedEpiMax = 8;
+__host__ __device__ constexpr int fused_epi(int cw) { return GF_FUSED_NE; }
 // CTA size for CW compute warps: + the epilogue warps + 1 producer warp
 __host__ __device__ constexpr int fused_threads(int cw) { return (cw + fused_epi(cw) + 1) * 32; }
 
@@ -59,14 +62,22 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned by
                : "memory");
 }
 
+// Waiting threads are suspended (up to this many ns, woken early when the
+// phase completes) instead of spinning, so blocked warps do not take issue
+// slots from the ones doing work on the same sub-partition.
+#ifndef GF_SUSPEND_NS
+#define GF_SUSPEND_NS 20000
+#endif
+constexpr unsigned kSuspendNs = GF_SUSPEND_NS;
+
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(kSuspendNs)
       : "memory");
   return ok != 0;
 }
@@ -74,6 +85,35 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
+}
+
+// The same on precomputed 32-bit shared addresses (no generic->shared
+// conversion per call in the hot loops).
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity), "r"(kSuspendNs)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ float4 lds128(uint32_t addr, float4*) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ double2 lds128(uint32_t addr, double2*) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
 }
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -102,19 +142,35 @@ __device__ __forceinline__ double vdot(const double2& a, const double2& b, doubl
   s = fma(a.x, b.x, s);
   return fma(a.y, b.y, s);
 }
+// fp32 rows use Blackwell's packed FFMA2 (fma.rn.f32x2): half the FMA
+// instructions of the scalar form for both passes.
 __device__ __forceinline__ void vaxpy(float4& acc, const float4& a, float w) {
-  acc.x = fmaf(a.x, w, acc.x);
-  acc.y = fmaf(a.y, w, acc.y);
-  acc.z = fmaf(a.z, w, acc.z);
-  acc.w = fmaf(a.w, w, acc.w);
+  const float2 ww = make_float2(w, w);
+  const float2 lo = __ffma2_rn(make_float2(a.x, a.y), ww, make_float2(acc.x, acc.y));
+  const float2 hi = __ffma2_rn(make_float2(a.z, a.w), ww, make_float2(acc.z, acc.w));
+  acc = make_float4(lo.x, lo.y, hi.x, hi.y);
 }
+// Row-pass dot accumulators: a float2 pair (even / odd lanes of the vector)
+// for fp32, a scalar for fp64.
+template <typename T> struct DotAcc;
+template <> struct DotAcc<float> { using type = float2; };
+template <> struct DotAcc<double> { using type = double; };
+__device__ __forceinline__ float2 dot_acc(const float4& a, const float4& b) {
+  const float2 s = __fmul2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));
+  return __ffma2_rn(make_float2(a.z, a.w), make_float2(b.z, b.w), s);
+}
+__device__ __forceinline__ double dot_acc(const double2& a, const double2& b) { return fma(a.y, b.y, a.x * b.x); }
+__device__ __forceinline__ float2 dot_add(float2 s, float2 t) { return make_float2(s.x + t.x, s.y + t.y); }
+__device__ __forceinline__ double dot_add(double s, double t) { return s + t; }
+__device__ __forceinline__ float dot_fin(float2 s) { return s.x + s.y; }
+__device__ __forceinline__ double dot_fin(double s) { return s; }
 __device__ __forceinline__ void vaxpy(double2& acc, const double2& a, double w) {
   acc.x = fma(a.x, w, acc.x);
   acc.y = fma(a.y, w, acc.y);
 }
 
 struct FusedPlan {
-  int cw = 0;        // compute warps (template instance: 16 or 20)
+  int cw = 0;        // compute warps (template instance: 8, 12, 16 or 20)
   int ne = 0;        // epilogue warps (= partial records per CTA)
   int nv = 0;        // 16-byte vectors per thread per row (template instance)
   int nslot = 0;     // rows resident in shared memory
@@ -128,11 +184,16 @@ inline FusedPlan plan_fused(int64_t m, int64_t ld, int esize, int sms, size_t sm
   FusedPlan p;
   const int vn = 16 / esize;
   const int64_t nvec = ld / vn;
-  // 20 compute warps when that lowers the vectors per thread (shorter
-  // per-warp critical path per row; registers still fit at 736 threads)
-  const int nv16 = (int)ceil_div(nvec, 16 * 32), nv20 = (int)ceil_div(nvec, 20 * 32);
-  p.cw = (nv20 < nv16 && nv20 <= 4) ? 20 : 16;
-  p.nv = p.cw == 20 ? nv20 : nv16;
+  // The fewest compute warps that keep the vectors per thread at <= 5
+  // (measured on B200, tools/fused_bench.cu: fewer, wider warps leave issue
+  // slots to the fp64 epilogue warps and cut the per-row sync overhead;
+  // 8 warps x 5 vectors beats 20 x 2 by 15 % on the 200000 x 5000 fp32 row).
+  // (16 and 20 compute warps: at most 4 vectors, the register budget of the
+  // larger CTA; beyond 20 x 4 the 5- and 6-vector instances spill a little)
+  p.cw = 20;
+  for (int cw : {8, 12, 16, 20})
+    if (ceil_div(nvec, cw * 32) <= (cw <= 12 ? 5 : 4)) { p.cw = cw; break; }
+  p.nv = (int)ceil_div(nvec, p.cw * 32);
   p.ne = fused_epi(p.cw);
   const size_t row_bytes = (size_t)ld * esize;
   const size_t budget = smem_max > 8192 ? smem_max - 8192 : 0;
@@ -257,7 +318,13 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
       const uint64_t pol = policy_evict_first();
       int slot = 0;
       for (int j = 0; j < nr; ++j) {
+#ifdef GF_FUSED_TRACE
+        long long c0 = clock64();
+#endif
         if (j >= nslot) mbar_wait(&sfree[slot], (unsigned)(((j / nslot) - 1) & 1));
+#ifdef GF_FUSED_TRACE
+        GF_TR_ADD(11, c0);
+#endif
         mbar_arrive_expect_tx(&full[slot], rb);
         bulk_g2s(smem_raw + slot * rb, A + (r0 + j) * ld, rb, &full[slot], pol);
         if (++slot == nslot) slot = 0;
@@ -348,24 +415,38 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
   }
 
   // ===================== compute warps =====================
+  // Thread tid owns the 16-byte column vectors c = tid + v * CW * 32.  Only
+  // the last (v = NV - 1) can fall past the row end (NV = ceil(nvec / (CW*32)));
+  // its smem index is clamped onto a vector of the same row (finite: A is
+  // validated finite) and its x entries are zero, so it adds exact zeros to
+  // the dots, and its column accumulators are never stored -- the inner loops
+  // carry no bounds branches.  All shared addresses are 32-bit and hoisted.
   V xa[NV], xb[NV], ca[NV], cb[NV];
-  bool valid[NV];
+  uint32_t voff[NV];
   {
     const V* xv0 = reinterpret_cast<const V*>(x0);
     const V* xv1 = reinterpret_cast<const V*>(x1);
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const int c = tid + v * kFusedThreads;
-      valid[v] = c < (int)nvec;
-      xa[v] = valid[v] ? xv0[c] : V{};
-      xb[v] = valid[v] ? xv1[c] : V{};
+      const bool ok = c < (int)nvec;
+      voff[v] = (uint32_t)(ok ? c : (int)nvec - 1) * 16u;
+      xa[v] = ok ? xv0[c] : V{};
+      xb[v] = ok ? xv1[c] : V{};
       ca[v] = V{};
       cb[v] = V{};
     }
   }
+  const uint32_t ring0 = smem_u32(smem_raw);
+  const uint32_t full0 = smem_u32(full), sfree0 = smem_u32(sfree);
+  const uint32_t redf0 = smem_u32(redf), rede0 = smem_u32(rede), wf0 = smem_u32(wf), we0 = smem_u32(we);
+  const bool red_writer = (lane & ((32 >> LGK) - 1)) == 0;
+  T* const red_dst = &red_s[0][warp][lane >> (5 - LGK)];   // + b * CW * K
   int slotR = 0, slotC = 0;
   unsigned phaseR = 0;
   int jR = 0, jC = 0;
+  int bR = 0, bC = 0;            // hand-off buffer of R(t) / C(t-2): t mod NE
+  unsigned useR = 0, useC = 0;   // its use count: t / NE
   for (int t = 0; t < ng + 2; ++t) {
     if (t < ng) {   // ---- R(t) ----
       T s[K];
@@ -377,66 +458,65 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
 #ifdef GF_FUSED_TRACE
           long long c0 = clock64();
 #endif
-          mbar_wait(&full[slotR], phaseR);
+          mbar_wait_u32(full0 + 8u * slotR, phaseR);
 #ifdef GF_FUSED_TRACE
           if (tid == 0) GF_TR_ADD(8, c0);
 #endif
-          const V* row = reinterpret_cast<const V*>(smem_raw + slotR * rb);
+          const uint32_t row = ring0 + (uint32_t)slotR * rb;
+          typename DotAcc<T>::type p0[NV], p1[NV];
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
-            if (valid[v]) {
-              const V a = row[tid + v * kFusedThreads];
-              s[2 * rr] = vdot(a, xa[v], s[2 * rr]);
-              s[2 * rr + 1] = vdot(a, xb[v], s[2 * rr + 1]);
-            }
+            const V a = lds128(row + voff[v], (V*)nullptr);
+            p0[v] = dot_acc(a, xa[v]);
+            p1[v] = dot_acc(a, xb[v]);
           }
+#pragma unroll
+          for (int v = 1; v < NV; ++v) { p0[0] = dot_add(p0[0], p0[v]); p1[0] = dot_add(p1[0], p1[v]); }
+          s[2 * rr] = dot_fin(p0[0]);
+          s[2 * rr + 1] = dot_fin(p1[0]);
           ++jR;
           if (++slotR == nslot) { slotR = 0; phaseR ^= 1u; }
         }
       }
       const T tot = warp_multi_sum<K>(s, lane);   // lane (q << (5-LGK)) holds value q
-      const int b = t % NE;
-      const unsigned use = (unsigned)(t / NE);
 #ifdef GF_FUSED_TRACE
       long long c0 = clock64();
 #endif
-      if (use >= 1) mbar_wait(&rede[b], (use - 1) & 1u);
+      if (useR >= 1) mbar_wait_u32(rede0 + 8u * bR, (useR - 1) & 1u);
 #ifdef GF_FUSED_TRACE
       if (tid == 0) GF_TR_ADD(9, c0);
 #endif
-      if ((lane & ((32 >> LGK) - 1)) == 0) red_s[b][warp][lane >> (5 - LGK)] = tot;
+      if (red_writer) red_dst[bR * (kFusedWarps * K)] = tot;
       __syncwarp();
-      if (lane == 0) mbar_arrive_expect_tx(&redf[b], 0);
+      if (lane == 0) mbar_arrive_u32(redf0 + 8u * bR);
+      if (++bR == NE) { bR = 0; ++useR; }
     }
     if (t >= 2) {   // ---- C(t-2) ----
-      const int b = (t - 2) % NE;
-      const unsigned use = (unsigned)((t - 2) / NE);
 #ifdef GF_FUSED_TRACE
       long long c0 = clock64();
 #endif
-      mbar_wait(&wf[b], use & 1u);
+      mbar_wait_u32(wf0 + 8u * bC, useC & 1u);
 #ifdef GF_FUSED_TRACE
       if (tid == 0) GF_TR_ADD(10, c0);
 #endif
       T w0[TR], w1[TR];
 #pragma unroll
-      for (int rr = 0; rr < TR; ++rr) { w0[rr] = w_s[b][rr][0]; w1[rr] = w_s[b][rr][1]; }
+      for (int rr = 0; rr < TR; ++rr) { w0[rr] = w_s[bC][rr][0]; w1[rr] = w_s[bC][rr][1]; }
       __syncwarp();
-      if (lane == 0) mbar_arrive_expect_tx(&we[b], 0);
+      if (lane == 0) mbar_arrive_u32(we0 + 8u * bC);
+      if (++bC == NE) { bC = 0; ++useC; }
 #pragma unroll
       for (int rr = 0; rr < TR; ++rr) {
         if (jC < nr) {
-          const V* row = reinterpret_cast<const V*>(smem_raw + slotC * rb);
+          const uint32_t row = ring0 + (uint32_t)slotC * rb;
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
-            if (valid[v]) {
-              const V a = row[tid + v * kFusedThreads];
-              vaxpy(ca[v], a, w0[rr]);
-              vaxpy(cb[v], a, w1[rr]);
-            }
+            const V a = lds128(row + voff[v], (V*)nullptr);
+            vaxpy(ca[v], a, w0[rr]);
+            vaxpy(cb[v], a, w1[rr]);
           }
           __syncwarp();
-          if (lane == 0) mbar_arrive_expect_tx(&sfree[slotC], 0);
+          if (lane == 0) mbar_arrive_u32(sfree0 + 8u * slotC);
           ++jC;
           if (++slotC == nslot) slotC = 0;
         }
@@ -447,7 +527,7 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     const int64_t c = tid + (int64_t)v * kFusedThreads;
-    if (valid[v]) {
+    if (c < nvec) {
       double* p0 = cpart + ((int64_t)blockIdx.x * 2) * ld + c * VN;
       double* p1 = cpart + ((int64_t)blockIdx.x * 2 + 1) * ld + c * VN;
 #pragma unroll

@@ -753,24 +753,34 @@ static void fused_tr(gf_solver* s, cudaStream_t st, bool attr_only) {
   }
 }
 
-// plan_fused picks 20 compute warps only for NV in {2, 3, 4}
+// plan_fused: CW = 8 for NV <= 5; 12 when 8 would need more (NV in {4, 5});
+// 16 and 20 for NV = 4; 20 with NV 5 or 6 for the widest fused rows
 template <typename T>
 static void fused_dispatch(gf_solver* s, cudaStream_t st, bool attr_only) {
-  if (s->fplan.cw == 20) {
-    switch (s->fplan.nv) {
-      case 2: fused_tr<T, 2, 20>(s, st, attr_only); break;
-      case 3: fused_tr<T, 3, 20>(s, st, attr_only); break;
-      default: fused_tr<T, 4, 20>(s, st, attr_only); break;
-    }
-    return;
-  }
-  switch (s->fplan.nv) {
-    case 1: fused_tr<T, 1, 16>(s, st, attr_only); break;
-    case 2: fused_tr<T, 2, 16>(s, st, attr_only); break;
-    case 3: fused_tr<T, 3, 16>(s, st, attr_only); break;
-    case 4: fused_tr<T, 4, 16>(s, st, attr_only); break;
-    case 5: fused_tr<T, 5, 16>(s, st, attr_only); break;
-    default: fused_tr<T, 6, 16>(s, st, attr_only); break;
+  const int nv = s->fplan.nv;
+  switch (s->fplan.cw) {
+    case 8:
+      switch (nv) {
+        case 1: fused_tr<T, 1, 8>(s, st, attr_only); break;
+        case 2: fused_tr<T, 2, 8>(s, st, attr_only); break;
+        case 3: fused_tr<T, 3, 8>(s, st, attr_only); break;
+        case 4: fused_tr<T, 4, 8>(s, st, attr_only); break;
+        default: fused_tr<T, 5, 8>(s, st, attr_only); break;
+      }
+      return;
+    case 12:
+      if (nv == 4) fused_tr<T, 4, 12>(s, st, attr_only); else fused_tr<T, 5, 12>(s, st, attr_only);
+      return;
+    case 16:
+      fused_tr<T, 4, 16>(s, st, attr_only);
+      return;
+    default:
+      switch (nv) {
+        case 4: fused_tr<T, 4, 20>(s, st, attr_only); break;
+        case 5: fused_tr<T, 5, 20>(s, st, attr_only); break;
+        default: fused_tr<T, 6, 20>(s, st, attr_only); break;
+      }
+      return;
   }
 }
 

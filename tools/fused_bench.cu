@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <algorithm>
+#include <functional>
 
 #include "gf_fused.cuh"
 #include "gf_terms.cuh"
@@ -242,8 +244,8 @@ float time_fused(const float* A, int64_t m, int64_t ld, const float* x0, const f
     for (int j = 0; j < 16; ++j) acc[j] += (double)tr[c * 16 + j] / 148.0 / 1965.0;   // us per CTA
   const double groups = (double)m / 148 / TR;
   printf("   per CTA (us): epi wait redf %.1f+%.1f | reduce %.1f | wait we %.1f | mid %.1f | tail+load %.1f | "
-         "epi total %.1f ;  compute w0: wait full %.1f rede %.1f wf %.1f   (groups %.0f, per group epi %.2f us)\n",
-         acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[8], acc[9], acc[10], groups,
+         "epi total %.1f ;  compute w0: wait full %.1f rede %.1f wf %.1f ; producer wait sfree %.1f  (groups %.0f, per group epi %.2f us)\n",
+         acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[8], acc[9], acc[10], acc[11], groups,
          (acc[2] + acc[3] + acc[4] + acc[5]) / groups);
 #endif
   return ms / reps;
@@ -331,17 +333,32 @@ int main(int argc, char** argv) {
       printf("epilogue alone (no loads), %2d busy warps: %.0f cycles per group\n", busy, (double)c / 600);
     }
   }
-  float ms;
-#define RUN(EPI, e, NV, TR, CW)                                                                     \
-  ms = time_fused<EPI, NV, TR, CW>(A, m, ld, x0, x1, e, p.nslot, rpart, cpart, reps, p.smem);       \
-  printf("fused %-9s NV=%d TR=%d CW=%d  %.4f ms  %.0f GB/s\n", #EPI, NV, TR, CW, ms, gb / ms * 1e3);
-  RUN(DummyEpi, de, 3, 2, 16)
-  RUN(DummyEpi, de, 2, 2, 20)
-  RUN(HeavyEpi, he, 3, 2, 16)
-  RUN(HeavyEpi, he, 2, 2, 20)
-  RUN(HeavyNoLoad, hn, 3, 2, 16)
-  RUN(HeavyNoLoad, hn, 2, 2, 20)
-  RUN(HeavyNoStore, hs, 3, 2, 16)
-  RUN(HeavyNoStore, hs, 2, 2, 20)
+  // configurations timed round-robin (clock / power drift hits all alike);
+  // min and median over rounds
+  struct Cfg { const char* name; std::function<float()> run; std::vector<float> t; };
+  std::vector<Cfg> cfgs;
+#define ADD(EPI, e, NV, TR, CW)                                                                          \
+  cfgs.push_back({#EPI " NV=" #NV " CW=" #CW, [&]() {                                                    \
+    return time_fused<EPI, NV, TR, CW>(A, m, ld, x0, x1, e, p.nslot, rpart, cpart, reps, p.smem); }, {}});
+  ADD(DummyEpi, de, 2, 2, 20)
+  ADD(DummyEpi, de, 3, 2, 16)
+  ADD(DummyEpi, de, 3, 2, 14)
+  ADD(DummyEpi, de, 4, 2, 12)
+  ADD(DummyEpi, de, 4, 2, 10)
+  ADD(DummyEpi, de, 5, 2, 8)
+  ADD(HeavyEpi, he, 2, 2, 20)
+  ADD(HeavyEpi, he, 3, 2, 16)
+  ADD(HeavyEpi, he, 3, 2, 14)
+  ADD(HeavyEpi, he, 4, 2, 12)
+  ADD(HeavyEpi, he, 4, 2, 10)
+  ADD(HeavyEpi, he, 5, 2, 8)
+  const int rounds = argc > 4 ? atoi(argv[4]) : 5;
+  for (int r = 0; r < rounds; ++r)
+    for (auto& c : cfgs) c.t.push_back(c.run());
+  for (auto& c : cfgs) {
+    std::sort(c.t.begin(), c.t.end());
+    printf("fused %-22s NE=%d  min %.4f ms (%.0f GB/s)  median %.4f ms\n", c.name, fused_epi(8), c.t[0],
+           gb / c.t[0] * 1e3, c.t[c.t.size() / 2]);
+  }
   return 0;
 }
