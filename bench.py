@@ -317,7 +317,7 @@ def run_ours(args):
     kms = (C.c_double * 8)()
     kcnt = (C.c_int64 * 8)()
     _native.check(L.gf_solver_stats(run.handle, None, kms, kcnt))
-    names = ["ginv_gemv_xside", "row_pass_yside", "col_pass", "slab_reduce", "y_scalars", "controller",
+    names = ["ginv_gemv_xside", "row_pass_yside", "col_pass", "slab_reduce", "y_scalars", "zstep_controller",
              "allreduce", "fused_rowcol_yside"]
     kernels = {names[i]: {"avg_ms": kms[i] / kcnt[i], "count": int(kcnt[i])} for i in range(8) if kcnt[i]}
     es = 4 if setup.dtype == _native.GF_F32 else 8

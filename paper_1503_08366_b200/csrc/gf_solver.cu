@@ -398,6 +398,64 @@ __device__ bool gap_test(Ctl* ctl, const Params& prm, const double* ys, const do
   return gap <= A_(prm.abs_tol, M_(prm.rel_tol, fabs(obj)));
 }
 
+// Thread 0 of the last controller CTA, tall orientation: stop rule, degenerate
+// checks, history row and adaptive rho of iteration k from the all-reduced y
+// scalars ys, the x-side sums xs (+ flags word) and r_dual^2.
+__device__ void decide_tall(Ctl* ctl, const Params& prm, const double* ys, const double* xs, double r2,
+                            double* hist) {
+  const int64_t k = ctl->k;
+  const unsigned xf = (unsigned)xs[kRedX];
+  const bool proj_bad = (xf & kBadXPlus) || ys[4] > 0.0;
+  const bool prox_bad = (xf & kBadXHalf) || ys[5] > 0.0;
+  if (k >= prm.max_iter) {  // past the last iteration: only its projection check remains
+    ctl->iterations = prm.max_iter;
+    if (proj_bad) { ctl->status = GF_STATUS_DEGENERATE; ctl->final_rho = ctl->rho_prev; }
+    else { ctl->status = GF_STATUS_MAX_ITERATIONS; ctl->final_rho = ctl->rho; }
+    return;
+  }
+  if (proj_bad || prox_bad) {   // solver.py:337-341 / :414-417 -> previous half iterate
+    ctl->status = GF_STATUS_DEGENERATE;
+    ctl->iterations = k;
+    ctl->final_rho = proj_bad ? ctl->rho_prev : ctl->rho;
+    return;
+  }
+  const double rho = ctl->rho;
+  const double r_pri = sqrt(ys[0]);
+  const double r_dual = sqrt(r2);
+  const double eps_pri = prm.abs_tol + prm.rel_tol * sqrt(ys[1]);
+  const double eps_dual = prm.abs_tol + prm.rel_tol * sqrt(xs[0]);
+  const double obj = ys[2] + xs[1];
+  double* hrow = hist + k * 8;
+  hrow[0] = r_pri; hrow[1] = r_dual; hrow[2] = eps_pri; hrow[3] = eps_dual;
+  hrow[4] = rho; hrow[5] = obj; hrow[6] = sqrt(ys[3] + xs[2]); hrow[7] = (double)ctl->inner;
+  ctl->last_good = k;
+  ctl->r_pri = r_pri; ctl->r_dual = r_dual; ctl->eps_pri = eps_pri; ctl->eps_dual = eps_dual;
+  ctl->objective = obj;
+  if ((r_pri <= eps_pri && r_dual <= eps_dual)       // solver.py:201, :373-376
+      || (prm.gap && gap_test(ctl, prm, ys, xs))) {   // solver.py:378-390
+    ctl->status = GF_STATUS_SOLVED;
+    ctl->iterations = k + 1;
+    ctl->final_rho = rho;
+    return;
+  }
+  double nrho = rho, ratio = 1.0;                  // adapt_rho, solver.py:221-239
+  if (prm.adaptive) {
+    if (r_dual < eps_dual && prm.tau * (double)k > (double)ctl->l_mark) {
+      nrho = prm.delta * rho;
+      ratio = rho / nrho;
+      ctl->u_mark = k;
+    } else if (r_pri < eps_pri && prm.tau * (double)k > (double)ctl->u_mark) {
+      nrho = rho / prm.delta;
+      ratio = rho / nrho;
+      ctl->l_mark = k;
+    }
+  }
+  ctl->rho_prev = rho;
+  ctl->rho = nrho;
+  ctl->ratio = ratio;
+  ctl->k = k + 1;
+}
+
 // Z2: per column the projection right-hand side (tall) or x+ (wide) and the
 // r_dual terms, then the controller in the last CTA.
 //   tall: red = [A_hat' c_y | A_hat' nu^ | y scalars]; rhs = c_x + A_hat' c_y
@@ -546,55 +604,171 @@ control_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ red
     ctl->k = k + 1;
     return;
   }
-  const bool proj_bad = (xf & kBadXPlus) || ys[4] > 0.0;
-  const bool prox_bad = (xf & kBadXHalf) || ys[5] > 0.0;
-  if (k >= prm.max_iter) {  // past the last iteration: only its projection check remains
-    ctl->iterations = prm.max_iter;
-    if (proj_bad) { ctl->status = GF_STATUS_DEGENERATE; ctl->final_rho = ctl->rho_prev; }
-    else { ctl->status = GF_STATUS_MAX_ITERATIONS; ctl->final_rho = ctl->rho; }
-    return;
+  decide_tall(ctl, prm, ys, xs, r2, hist);
+}
+
+// Z(k) in one launch for tall problems without a communicator: the column
+// slab reduce, the y-scalar reduce and the controller (replaces colreduce +
+// y_scalars + control_kernel).  CTA b owns columns [32 b, 32 b + 32): warp w
+// sums slabs w, w + 8, ... of both column partials (fixed order, coalesced
+// 256-byte rows), the 8 warp partials are added in warp order, then lane j of
+// warp 0 forms rhs_j = c_x + A_hat' c_y and the r_dual term of its column.
+// The last CTA (ticket) reduces the y records (rpart), the x records (xpart)
+// and the per-CTA r_dual partials, all in fixed order, and runs the
+// controller.  Deterministic: same sums in the same order on every run.
+template <int K>
+__device__ void block_sum_records(const double* __restrict__ rec, int64_t count, double (&out)[K + 1],
+                                  double (*sh)[K + 1]) {
+  // rec: count records of K sums + 1 flags word; out: the K sums + OR of flags
+  double v[K + 1];
+#pragma unroll
+  for (int q = 0; q <= K; ++q) v[q] = 0.0;
+  unsigned fl = 0;
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) {
+#pragma unroll
+    for (int q = 0; q < K; ++q) v[q] += rec[i * (K + 1) + q];
+    fl |= (unsigned)rec[i * (K + 1) + K];
   }
-  if (proj_bad || prox_bad) {   // solver.py:337-341 / :414-417 -> previous half iterate
-    ctl->status = GF_STATUS_DEGENERATE;
-    ctl->iterations = k;
-    ctl->final_rho = proj_bad ? ctl->rho_prev : ctl->rho;
-    return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < K; ++q) v[q] = warp_sum(v[q]);
+  fl = warp_or(fl);
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < K; ++q) sh[warp][q] = v[q];
+    sh[warp][K] = (double)fl;
   }
-  const double rho = ctl->rho;
-  const double r_pri = sqrt(ys[0]);
-  const double r_dual = sqrt(r2);
-  const double eps_pri = prm.abs_tol + prm.rel_tol * sqrt(ys[1]);
-  const double eps_dual = prm.abs_tol + prm.rel_tol * sqrt(xs[0]);
-  const double obj = ys[2] + xs[1];
-  double* hrow = hist + k * 8;
-  hrow[0] = r_pri; hrow[1] = r_dual; hrow[2] = eps_pri; hrow[3] = eps_dual;
-  hrow[4] = rho; hrow[5] = obj; hrow[6] = sqrt(ys[3] + xs[2]); hrow[7] = (double)ctl->inner;
-  ctl->last_good = k;
-  ctl->r_pri = r_pri; ctl->r_dual = r_dual; ctl->eps_pri = eps_pri; ctl->eps_dual = eps_dual;
-  ctl->objective = obj;
-  if ((r_pri <= eps_pri && r_dual <= eps_dual)       // solver.py:201, :373-376
-      || (prm.gap && gap_test(ctl, prm, ys, xs))) {   // solver.py:378-390
-    ctl->status = GF_STATUS_SOLVED;
-    ctl->iterations = k + 1;
-    ctl->final_rho = rho;
-    return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      double t = 0.0;
+      for (int w = 0; w < nw; ++w) t += sh[w][q];
+      out[q] = t;
+    }
+    unsigned f = 0;
+    for (int w = 0; w < nw; ++w) f |= (unsigned)sh[w][K];
+    out[K] = (double)f;
   }
-  double nrho = rho, ratio = 1.0;                  // adapt_rho, solver.py:221-239
-  if (prm.adaptive) {
-    if (r_dual < eps_dual && prm.tau * (double)k > (double)ctl->l_mark) {
-      nrho = prm.delta * rho;
-      ratio = rho / nrho;
-      ctl->u_mark = k;
-    } else if (r_pri < eps_pri && prm.tau * (double)k > (double)ctl->u_mark) {
-      nrho = rho / prm.delta;
-      ratio = rho / nrho;
-      ctl->l_mark = k;
+  __syncthreads();
+}
+
+// Column sums of the slab partials for columns [c0, c0 + 32): warp w adds
+// slabs w, w + 8, ...; the 8 warp partials are added in warp order.  Result
+// in lane j of warp 0 (s1, s2).  Every CTA thread must call it.
+__device__ __forceinline__ void slab_columns(const double* __restrict__ cpart, int64_t slabs, int64_t ld, int64_t n,
+                                             int64_t c0, double (*part)[2][33], double& s1, double& s2) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t j = c0 + lane;
+  s1 = 0.0;
+  s2 = 0.0;
+  if (j < n)
+    for (int64_t sl = warp; sl < slabs; sl += 8) {
+      s1 += cpart[(2 * sl) * ld + j];
+      s2 += cpart[(2 * sl + 1) * ld + j];
+    }
+  part[warp][0][lane] = s1;
+  part[warp][1][lane] = s2;
+  __syncthreads();
+  if (warp == 0) {
+    s1 = part[0][0][lane];
+    s2 = part[0][1][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) { s1 += part[w][0][lane]; s2 += part[w][1][lane]; }
+  }
+  __syncthreads();
+}
+
+// The y records in the controller's scalar layout (see y_scalars_kernel):
+// [r_pri^2, ||y||^2, f(y), drift_y^2, bad y+, bad y_1/2, f(y_full), f*(nu_full)]
+__device__ __forceinline__ void y_layout(const double (&yr)[kRedY + 1], double* ys) {
+  const unsigned yf = (unsigned)yr[kRedY];
+  ys[0] = yr[0]; ys[1] = yr[1]; ys[2] = yr[2]; ys[3] = yr[3];
+  ys[4] = (yf & kBadYPlus) ? 1.0 : 0.0;
+  ys[5] = (yf & kBadYHalf) ? 1.0 : 0.0;
+  ys[6] = yr[4]; ys[7] = yr[5];
+}
+
+// Row-partitioned runs: the same reductions as zslab_tall_kernel<true>, in the
+// same order, written to red = [A' c_y | A' nu^ | y scalars] for the
+// all-reduce; zslab_tall_kernel<false> then reads them.  With one rank the
+// result is bit-identical to the communicator-free path.
+__global__ void __launch_bounds__(256)
+zreduce_kernel(const Ctl* __restrict__ ctl, const double* __restrict__ cpart, int64_t slabs, int64_t ld, int64_t n,
+               const double* __restrict__ rpart, int64_t nrpart, double* __restrict__ red) {
+  if (ctl->status != GF_STATUS_RUNNING) return;
+  __shared__ double part[8][2][33];
+  __shared__ double shr[8][kRedY + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t c0 = (int64_t)blockIdx.x * 32; c0 < ld; c0 += (int64_t)gridDim.x * 32) {
+    double s1, s2;
+    slab_columns(cpart, slabs, ld, ld, c0, part, s1, s2);
+    if (warp == 0 && c0 + lane < ld) {
+      red[c0 + lane] = s1;
+      red[ld + c0 + lane] = s2;
     }
   }
-  ctl->rho_prev = rho;
-  ctl->rho = nrho;
-  ctl->ratio = ratio;
-  ctl->k = k + 1;
+  if (blockIdx.x == 0) {
+    double yr[kRedY + 1];
+    block_sum_records<kRedY>(rpart, nrpart, yr, shr);
+    if (threadIdx.x == 0) y_layout(yr, red + 2 * ld);
+  }
+}
+
+template <typename T, bool FROM_SLABS>
+__global__ void __launch_bounds__(256)
+zslab_tall_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ cpart, int64_t slabs, int64_t ld,
+                  int64_t n, const double* __restrict__ rpart, int64_t nrpart, const double* __restrict__ cx,
+                  const double* __restrict__ e, const double* __restrict__ muh2, T* __restrict__ rhs_T,
+                  double* __restrict__ zpart, const double* __restrict__ xpart, int64_t nxpart,
+                  double* __restrict__ hist, double* __restrict__ red) {
+  if (ctl->status != GF_STATUS_RUNNING) return;
+  __shared__ double part[8][2][33];
+  __shared__ double shr[8][kRedY + 1];
+  __shared__ double shx[8][kRedX + 1];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t k = ctl->k;
+  const double* muh = muh2 + (k & 1) * n;
+  double rd2 = 0.0;
+  for (int64_t c0 = (int64_t)blockIdx.x * 32; c0 < n; c0 += (int64_t)gridDim.x * 32) {
+    const int64_t j = c0 + lane;
+    double s1 = 0.0, s2 = 0.0;
+    if (FROM_SLABS) {
+      slab_columns(cpart, slabs, ld, n, c0, part, s1, s2);
+    } else if (j < n) {
+      s1 = red[j];
+      s2 = red[ld + j];
+    }
+    if (warp == 0 && j < n) {
+      rhs_T[j] = (T)A_(cx[j], s1);                      // c + A_hat' d (projection.py:121)
+      const double ej = e[j];
+      const double rdj = A_(D_(s2, ej), D_(muh[j], ej));  // A' nu + mu in original space
+      rd2 += rdj * rdj;
+    }
+  }
+  if (warp == 0) {
+    rd2 = warp_sum(rd2);
+    if (lane == 0) {
+      zpart[blockIdx.x] = rd2;
+      __threadfence();
+      last = atomicAdd(&ctl->ticket, 1u) == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double yr[kRedY + 1], xs[kRedX + 1];
+  if (FROM_SLABS) block_sum_records<kRedY>(rpart, nrpart, yr, shr);
+  block_sum_records<kRedX>(xpart, nxpart, xs, shx);
+  if (threadIdx.x != 0) return;
+  double r2 = 0.0;
+  for (unsigned b = 0; b < gridDim.x; ++b) r2 += zpart[b];
+  ctl->ticket = 0;
+  double* ys = red + 2 * ld;
+  if (FROM_SLABS) y_layout(yr, ys);
+  decide_tall(ctl, prm, ys, xs, r2, hist);
 }
 
 // ------------------------------------------------------------- results --
@@ -665,7 +839,7 @@ struct gf_solver {
   DBuf xk, xt, cx, xh2, muh2, yk, yt, cy, yh2, nuh2;
   DBuf xk_T, xh_T, rhs_T;
   DBuf rpart, cpart, red, zpart, xpart;
-  int64_t grid_r = 1, grid_s = 1, grid_z = 1;
+  int64_t grid_r = 1, grid_s = 1, grid_z = 1, grid_zt = 1;
   ColPlan cplan;
   FusedPlan fplan;
   int warm_x = 0;
@@ -863,16 +1037,23 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
       nrpart = s->grid_r;
       s->launches += 2;
     }
+    if (!comm_active(s->S->comm)) {   // Z(k) in one launch: slab + y reduce + controller
+      s->mark(5, st, true);
+      zslab_tall_kernel<T, true><<<(unsigned)s->grid_zt, 256, 0, st>>>(
+          ctl, s->prm, s->cpart.as<double>(), slabs, s->ld, s->n, s->rpart.as<double>(), nrpart,
+          s->cx.as<double>(), s->S->e.as<double>(), s->muh2.as<double>(), s->rhs_T.as<T>(), s->zpart.as<double>(),
+          s->xpart.as<double>(), s->grid_s, s->hist.as<double>(), s->red.as<double>());
+      GF_CHECK_LAUNCH();
+      s->mark(5, st, false);
+      s->launches += 1;
+      return;
+    }
     s->mark(3, st, true);
-    colreduce_kernel<<<dim3((unsigned)ceil_div(s->ld, 32), 2), dim3(32, 8), 0, st>>>(
-        s->cpart.as<double>(), slabs, s->ld, 2, s->red.as<double>(), &ctl->status);
+    zreduce_kernel<<<(unsigned)s->grid_zt, 256, 0, st>>>(ctl, s->cpart.as<double>(), slabs, s->ld, s->n,
+                                                          s->rpart.as<double>(), nrpart, s->red.as<double>());
     GF_CHECK_LAUNCH();
     s->mark(3, st, false);
-    s->mark(4, st, true);
-    y_scalars_kernel<<<1, 256, 0, st>>>(s->rpart.as<double>(), nrpart, s->red.as<double>() + 2 * s->ld, ctl);
-    GF_CHECK_LAUNCH();
-    s->mark(4, st, false);
-    s->launches += 2;
+    s->launches += 1;
   } else {
     GF_CUDA(cudaMemsetAsync(s->red.p, 0, (2 * s->ld + kScal) * sizeof(double), st));
   }
@@ -882,9 +1063,10 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
     s->mark(6, st, false);
   }
   s->mark(5, st, true);
-  control_kernel<T, false><<<(unsigned)s->grid_z, 256, 0, st>>>(
-      ctl, s->prm, s->red.as<double>(), s->ld, s->n, s->cx.as<double>(), s->S->e.as<double>(), s->muh2.as<double>(),
-      s->rhs_T.as<T>(), s->zpart.as<double>(), s->xpart.as<double>(), s->grid_s, s->hist.as<double>(), nullptr, 0);
+  zslab_tall_kernel<T, false><<<(unsigned)s->grid_zt, 256, 0, st>>>(
+      ctl, s->prm, nullptr, 0, s->ld, s->n, nullptr, 0, s->cx.as<double>(), s->S->e.as<double>(),
+      s->muh2.as<double>(), s->rhs_T.as<T>(), s->zpart.as<double>(), s->xpart.as<double>(), s->grid_s,
+      s->hist.as<double>(), s->red.as<double>());
   GF_CHECK_LAUNCH();
   s->mark(5, st, false);
   s->launches += 1;
@@ -1031,6 +1213,7 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
   s->grid_r = row_grid(m1, sms);
   s->grid_s = row_grid(s->q, sms);
   s->grid_z = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 2 * (int64_t)sms));
+  s->grid_zt = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 32), 4 * (int64_t)sms));
   s->cplan = plan_cols(m1, s->ld, s->dtype == GF_F32 ? 4 : 2, sms);
   auto vec = [&](DBuf& b, int64_t len) { b.alloc(len * sizeof(double)); GF_CUDA(cudaMemsetAsync(b.p, 0, b.bytes, st)); };
   vec(s->xk, n); vec(s->xt, n); vec(s->cx, n); vec(s->xh2, 2 * n); vec(s->muh2, 2 * n);
@@ -1052,7 +1235,7 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
   const int64_t nslab = std::max<int64_t>(s->cplan.slabs, s->fplan.ok ? s->fplan.grid : 1);
   vec(s->rpart, std::max<int64_t>(s->grid_r, s->fplan.ok ? kFusedEpiMax * s->fplan.grid : 1) * (kRedY + 1));
   vec(s->xpart, s->grid_s * (kRedX + 1));
-  vec(s->zpart, s->grid_z);
+  vec(s->zpart, std::max(s->grid_z, s->grid_zt));
   vec(s->red, 2 * s->ld + kScal);
   if (!s->tall) {
     vec(s->ypl, m1);

@@ -22,7 +22,7 @@ CONFIGS = {
     "c3": ("lp", 50_000, 20_000, np.float64),
     "c4": ("svm", 200_000, 5_000, np.float32),
 }
-NAMES = ["ginv_gemv_xside", "row_pass_yside", "col_pass", "slab_reduce", "y_scalars", "controller",
+NAMES = ["ginv_gemv_xside", "row_pass_yside", "col_pass", "slab_reduce", "y_scalars", "zstep_controller",
          "allreduce", "fused_rowcol_yside"]
 
 
