@@ -50,6 +50,7 @@ struct PhaseTimer {
   cudaStream_t st;
   bool on;
   std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  std::vector<double> host_ms;   // host clock at each mark (enqueue time)
   explicit PhaseTimer(cudaStream_t s) : st(s) {
     const char* e = getenv("GF_VERBOSE_SETUP");
     on = e && e[0] == '1';
@@ -61,6 +62,8 @@ struct PhaseTimer {
     cudaEventCreate(&ev);
     cudaEventRecord(ev, st);
     marks.emplace_back(name, ev);
+    host_ms.push_back(std::chrono::duration<double, std::milli>(
+                          std::chrono::steady_clock::now().time_since_epoch()).count());
   }
   void report(const char* what) {
     if (!on) return;
@@ -69,7 +72,7 @@ struct PhaseTimer {
     for (size_t i = 1; i < marks.size(); ++i) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
-      fprintf(stderr, " %s %.2f ms", marks[i].first.c_str(), ms);
+      fprintf(stderr, " %s %.2f ms (host %.2f)", marks[i].first.c_str(), ms, host_ms[i] - host_ms[i - 1]);
     }
     fprintf(stderr, "\n");
   }

@@ -153,63 +153,140 @@ void gram_finish(double* G, int64_t q, int64_t ldg, cudaStream_t st) {
 // ---------------------------------------------------- blocked Cholesky ----
 constexpr int NB = 64;
 
-// Factor the nb x nb diagonal block at (k0, k0) in shared memory.
-__global__ void potrf_diag(double* G, int64_t ld, int64_t k0, int nb, int* info) {
-  __shared__ double S[NB][NB + 1];
-  const int tid = threadIdx.x;
+// Blocked right-looking Cholesky with 128-wide blocks (40 steps at q = 5000):
+//   potrf_block  one CTA factors the diagonal block in shared memory, itself
+//                right-looking over 16-column micro-panels (warp-level 16x16
+//                factor, per-row forward substitution, 4x4 register-blocked
+//                trailing update);
+//   trsm_rows    one warp per panel row below it, X <- X L_kk^-T, the row in
+//                registers (4 columns per lane), L_kk in shared memory;
+//   gemm         trailing update G22 -= L21 L21' (lower tiles only).
+constexpr int CB = 128, CMB = 16, CSL = CB + 1;
+constexpr size_t kCholSmem = (size_t)CB * CSL * sizeof(double);
+
+__global__ void __launch_bounds__(512) potrf_block(double* G, int64_t ld, int64_t k0, int nb, int* info) {
+  extern __shared__ double S[];
+  __shared__ double rinv[CB];   // reciprocals of the finished pivots (no divisions in the chains)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
     const int i = idx / nb, j = idx % nb;
-    S[i][j] = G[(k0 + i) * ld + k0 + j];
+    if (j <= i) S[i * CSL + j] = G[(k0 + i) * ld + k0 + j];
   }
   __syncthreads();
-  for (int j = 0; j < nb; ++j) {
-    if (tid == 0) {
-      const double dj = S[j][j];
-      if (!(dj > 0.0) || !isfinite(dj)) {
-        if (*info == 0) *info = (int)(k0 + j + 1);
-        S[j][j] = 1.0;
-      } else {
-        S[j][j] = sqrt(dj);
+  for (int p = 0; p < nb; p += CMB) {
+    const int w = min(CMB, nb - p);
+    if (warp == 0) {   // w x w diagonal piece, lane i <-> row p + i
+      for (int j = 0; j < w; ++j) {
+        double* dj = &S[(p + j) * CSL + p + j];
+        if (lane == 0) {
+          const double v = *dj;
+          if (!(v > 0.0) || !isfinite(v)) {
+            if (*info == 0) *info = (int)(k0 + p + j + 1);
+            *dj = 1.0;
+          } else {
+            *dj = sqrt(v);
+          }
+          rinv[p + j] = 1.0 / *dj;
+        }
+        __syncwarp();
+        const double ri = rinv[p + j];
+        if (lane > j && lane < w) S[(p + lane) * CSL + p + j] *= ri;
+        __syncwarp();
+        if (lane > j && lane < w) {
+          const double lij = S[(p + lane) * CSL + p + j];
+          for (int k = j + 1; k <= lane; ++k) S[(p + lane) * CSL + p + k] -= lij * S[(p + k) * CSL + p + j];
+        }
+        __syncwarp();
       }
     }
     __syncthreads();
-    const double piv = S[j][j];
-    for (int i = j + 1 + tid; i < nb; i += blockDim.x) S[i][j] /= piv;
+    const int rows = nb - p - w;
+    for (int rr = tid; rr < rows; rr += blockDim.x) {   // X <- X L_pp^-T
+      double* x = S + (p + w + rr) * CSL + p;
+      for (int c = 0; c < w; ++c) {
+        double sacc = x[c];
+        for (int t = 0; t < c; ++t) sacc -= x[t] * S[(p + c) * CSL + p + t];
+        x[c] = sacc * rinv[p + c];
+      }
+    }
     __syncthreads();
-    const int rem = nb - j - 1;
-    for (int idx = tid; idx < rem * rem; idx += blockDim.x) {
-      const int i = j + 1 + idx / rem, k = j + 1 + idx % rem;
-      if (k <= i) S[i][k] -= S[i][j] * S[k][j];
+    const int nt = (rows + 3) / 4;   // trailing lower update, 4x4 tiles
+    const int ntiles = nt * (nt + 1) / 2;
+    for (int ti = tid; ti < ntiles; ti += blockDim.x) {
+      int bi = (int)((sqrtf(8.f * ti + 1.f) - 1.f) * 0.5f);
+      while ((bi + 1) * (bi + 2) / 2 <= ti) ++bi;
+      while (bi * (bi + 1) / 2 > ti) --bi;
+      const int bj = ti - bi * (bi + 1) / 2;
+      const int i0 = p + w + 4 * bi, j0 = p + w + 4 * bj;
+      double acc[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+      for (int t = 0; t < w; ++t) {
+        double a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a[u] = i0 + u < nb ? S[(i0 + u) * CSL + p + t] : 0.0;
+          b[u] = j0 + u < nb ? S[(j0 + u) * CSL + p + t] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          if (i0 + u < nb && j0 + v <= i0 + u) S[(i0 + u) * CSL + j0 + v] -= acc[u][v];
     }
     __syncthreads();
   }
   for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
     const int i = idx / nb, j = idx % nb;
-    G[(k0 + i) * ld + k0 + j] = j <= i ? S[i][j] : 0.0;
+    G[(k0 + i) * ld + k0 + j] = j <= i ? S[i * CSL + j] : 0.0;
   }
 }
 
-// Panel: rows r >= k0+nb, columns [k0, k0+nb): X <- X * Lkk^-T.
-// One thread per row; the row lives in a thread-local array.
-__global__ void trsm_panel(double* G, int64_t ld, int64_t q, int64_t k0, int nb) {
-  __shared__ double L[NB][NB + 1];
-  const int tid = threadIdx.x;
+// Panel rows r >= k0 + nb: x <- x L_kk^-T, one warp per row; lane l holds
+// columns l, l + 32, l + 64, l + 96 of x.  Column c is finished by the lane
+// owning it, broadcast, and subtracted from the later columns (right-looking).
+__global__ void __launch_bounds__(512) trsm_rows(double* G, int64_t ld, int64_t q, int64_t k0, int nb) {
+  extern __shared__ double Ls[];
+  __shared__ double rinv[CB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
     const int i = idx / nb, j = idx % nb;
-    L[i][j] = G[(k0 + i) * ld + k0 + j];
+    if (j <= i) Ls[i * CSL + j] = G[(k0 + i) * ld + k0 + j];
   }
+  for (int c = tid; c < nb; c += blockDim.x) rinv[c] = 1.0 / G[(k0 + c) * ld + k0 + c];
   __syncthreads();
-  const int64_t r = k0 + nb + (int64_t)blockIdx.x * blockDim.x + tid;
-  if (r >= q) return;
-  double x[NB];
-  double* row = G + r * ld + k0;
-  for (int c = 0; c < nb; ++c) x[c] = row[c];
-  for (int c = 0; c < nb; ++c) {
-    double s = x[c];
-    for (int t = 0; t < c; ++t) s -= x[t] * L[c][t];
-    x[c] = s / L[c][c];
+  const int nw = blockDim.x >> 5;
+  for (int64_t r = k0 + nb + (int64_t)blockIdx.x * nw + warp; r < q; r += (int64_t)gridDim.x * nw) {
+    double* row = G + r * ld + k0;
+    double x[CB / 32];
+#pragma unroll
+    for (int i = 0; i < CB / 32; ++i) x[i] = lane + 32 * i < nb ? row[lane + 32 * i] : 0.0;
+#pragma unroll
+    for (int sl = 0; sl < CB / 32; ++sl) {
+      for (int o = 0; o < 32; ++o) {
+        const int c = 32 * sl + o;
+        if (c >= nb) break;
+        double xc = __shfl_sync(0xffffffffu, x[sl], o);
+        xc *= rinv[c];
+        if (lane == o) x[sl] = xc;
+#pragma unroll
+        for (int i = 0; i < CB / 32; ++i) {
+          const int t = lane + 32 * i;
+          if (t > c && t < nb) x[i] -= xc * Ls[t * CSL + c];
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < CB / 32; ++i)
+      if (lane + 32 * i < nb) row[lane + 32 * i] = x[i];
   }
-  for (int c = 0; c < nb; ++c) row[c] = x[c];
 }
 
 __global__ void zero_upper(double* G, int64_t q, int64_t ld) {
@@ -221,14 +298,23 @@ __global__ void zero_upper(double* G, int64_t q, int64_t ld) {
 // In-place lower Cholesky of G (fp64, q x q, row stride ld); upper part zeroed.
 // Returns 0 or the 1-based index of the first non-positive pivot.
 int cholesky(double* G, int64_t q, int64_t ld, int* d_info, cudaStream_t st) {
+  GF_CUDA(cudaFuncSetAttribute(potrf_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCholSmem));
+  GF_CUDA(cudaFuncSetAttribute(trsm_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCholSmem));
+  int sms = 148;
+  {
+    int dev = 0;
+    GF_CUDA(cudaGetDevice(&dev));
+    GF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
   GF_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), st));
-  for (int64_t k0 = 0; k0 < q; k0 += NB) {
-    const int nb = (int)std::min<int64_t>(NB, q - k0);
-    potrf_diag<<<1, 256, 0, st>>>(G, ld, k0, nb, d_info);
+  for (int64_t k0 = 0; k0 < q; k0 += CB) {
+    const int nb = (int)std::min<int64_t>(CB, q - k0);
+    potrf_block<<<1, 512, kCholSmem, st>>>(G, ld, k0, nb, d_info);
     GF_CHECK_LAUNCH();
     const int64_t rest = q - k0 - nb;
     if (rest <= 0) break;
-    trsm_panel<<<(unsigned)ceil_div(rest, 128), 128, 0, st>>>(G, ld, q, k0, nb);
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(rest, 16), sms);
+    trsm_rows<<<grid, 512, kCholSmem, st>>>(G, ld, q, k0, nb);
     GF_CHECK_LAUNCH();
     double* L21 = G + (k0 + nb) * ld + k0;
     double* G22 = G + (k0 + nb) * ld + k0 + nb;
