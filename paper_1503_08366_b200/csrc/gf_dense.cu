@@ -16,6 +16,8 @@
 // O(m q^2) Gram.  The Gram itself reads the working-dtype matrix and
 // accumulates in fp64.
 
+#include <vector>
+
 #include "gf_internal.h"
 
 namespace gf {
@@ -175,6 +177,54 @@ __global__ void __launch_bounds__(512) potrf_block(double* G, int64_t ld, int64_
   __syncthreads();
   for (int p = 0; p < nb; p += CMB) {
     const int w = min(CMB, nb - p);
+    if (w == CMB) {
+      if (warp == 0) {   // full 16 x 16 leaf in registers: lane i holds row p + i
+        double r[CMB];
+#pragma unroll
+        for (int k = 0; k < CMB; ++k) r[k] = (lane < CMB && k <= lane) ? S[(p + lane) * CSL + p + k] : 0.0;
+#pragma unroll
+        for (int j = 0; j < CMB; ++j) {
+          double dj = __shfl_sync(0xffffffffu, r[j], j);
+          if (!(dj > 0.0) || !isfinite(dj)) {
+            if (lane == 0 && *info == 0) *info = (int)(k0 + p + j + 1);
+            dj = 1.0;
+          } else {
+            dj = sqrt(dj);
+          }
+          const double ri = 1.0 / dj;
+          if (lane == j) r[j] = dj;
+          if (lane > j) r[j] *= ri;
+          if (lane == 0) rinv[p + j] = ri;
+#pragma unroll
+          for (int k = j + 1; k < CMB; ++k) {
+            const double lkj = __shfl_sync(0xffffffffu, r[j], k);
+            if (lane >= k) r[k] = fma(-r[j], lkj, r[k]);
+          }
+        }
+        if (lane < CMB)
+#pragma unroll
+          for (int k = 0; k < CMB; ++k)
+            if (k <= lane) S[(p + lane) * CSL + p + k] = r[k];
+      }
+      __syncthreads();
+      const int rows = nb - p - CMB;
+      for (int rr = tid; rr < rows; rr += blockDim.x) {   // X <- X L_pp^-T, row in registers
+        double* xs = S + (p + CMB + rr) * CSL + p;
+        double x[CMB];
+#pragma unroll
+        for (int c = 0; c < CMB; ++c) x[c] = xs[c];
+#pragma unroll
+        for (int c = 0; c < CMB; ++c) {
+          double sacc = x[c];
+#pragma unroll
+          for (int t = 0; t < c; ++t) sacc = fma(-x[t], S[(p + c) * CSL + p + t], sacc);
+          x[c] = sacc * rinv[p + c];
+        }
+#pragma unroll
+        for (int c = 0; c < CMB; ++c) xs[c] = x[c];
+      }
+      __syncthreads();
+    } else {
     if (warp == 0) {   // w x w diagonal piece, lane i <-> row p + i
       for (int j = 0; j < w; ++j) {
         double* dj = &S[(p + j) * CSL + p + j];
@@ -210,6 +260,8 @@ __global__ void __launch_bounds__(512) potrf_block(double* G, int64_t ld, int64_
       }
     }
     __syncthreads();
+    }
+    const int rows = nb - p - w;
     const int nt = (rows + 3) / 4;   // trailing lower update, 4x4 tiles
     const int ntiles = nt * (nt + 1) / 2;
     for (int ti = tid; ti < ntiles; ti += blockDim.x) {
@@ -307,18 +359,44 @@ int cholesky(double* G, int64_t q, int64_t ld, int* d_info, cudaStream_t st) {
     GF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   GF_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), st));
+  const char* vb = getenv("GF_VERBOSE_SETUP");
+  const bool prof = vb && vb[0] == '1';
+  std::vector<cudaEvent_t> ev;
+  auto mark = [&]() {
+    if (!prof) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.push_back(e);
+  };
+  mark();
   for (int64_t k0 = 0; k0 < q; k0 += CB) {
     const int nb = (int)std::min<int64_t>(CB, q - k0);
     potrf_block<<<1, 512, kCholSmem, st>>>(G, ld, k0, nb, d_info);
     GF_CHECK_LAUNCH();
+    mark();
     const int64_t rest = q - k0 - nb;
     if (rest <= 0) break;
     const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(rest, 16), sms);
     trsm_rows<<<grid, 512, kCholSmem, st>>>(G, ld, q, k0, nb);
     GF_CHECK_LAUNCH();
+    mark();
     double* L21 = G + (k0 + nb) * ld + k0;
     double* G22 = G + (k0 + nb) * ld + k0 + nb;
     gemm<double, double, false, true>(rest, rest, nb, -1.0, L21, ld, L21, ld, 1.0, G22, ld, true, st);
+    mark();
+  }
+  if (prof) {
+    GF_CUDA(cudaStreamSynchronize(st));
+    double t[3] = {0, 0, 0};
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      t[(i - 1) % 3] += ms;
+    }
+    fprintf(stderr, "[gf] cholesky q=%lld: potrf %.2f ms, trsm %.2f ms, update %.2f ms\n", (long long)q, t[0], t[1],
+            t[2]);
+    for (auto e : ev) cudaEventDestroy(e);
   }
   zero_upper<<<grid2(q), dim3(32, 8), 0, st>>>(G, q, ld);
   GF_CHECK_LAUNCH();

@@ -24,6 +24,9 @@
 // by tcgen05.commit) and 2 TMEM accumulators (256 columns each; full by
 // tcgen05.commit, empty by the epilogue warps).
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "gf_internal.h"
 
 namespace gf {
@@ -32,7 +35,7 @@ namespace syrk {
 // K-major, no-swizzle operand layout (verified on B200 with tools/umma_probe.cu):
 // a core matrix is 8 MN-rows x 16 bytes (4 tf32 along K), 128 contiguous
 // bytes; 8-row groups are SBO = 128 B apart, 4-element K chunks LBO apart.
-constexpr int TM = 128, TN = 256, BK = 16, NST = 4;
+constexpr int TM = 128, TN = 256, BK = 16, NST = 2;
 // rows per TMEM accumulation: 512 -> max |G error| / max |G| ~ 4.7e-6 on a
 // 20000 x 1300 Gaussian matrix (1024: 9.5e-6, 128: 1.2e-6; tools/syrk_accuracy.py)
 constexpr int KCHUNK_DEFAULT = 512;
@@ -41,9 +44,16 @@ constexpr int B_BYTES = (BK / 4) * (TN / 8) * 128; // 16 KB per hi/lo
 constexpr int LBO_A = (TM / 8) * 128;              // K-chunk stride
 constexpr int LBO_B = (TN / 8) * 128;
 constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;   // 48 KB
-constexpr int SMEM = NST * STAGE;                  // 192 KB
-constexpr int NPROD = 8;                           // producer warps
-constexpr int THREADS = (5 + NPROD) * 32;
+constexpr int NPROD = 8;                           // converter warps
+constexpr int LOADER_WARP = 5 + NPROD;             // TMA loader warp
+constexpr int THREADS = (6 + NPROD) * 32;
+// raw fp32 ring filled by 2-D tensor TMA: per stage two boxes, BK rows x TM
+// columns (A panel, 8 KB) then BK rows x TN columns (B panel, 16 KB), rows
+// and columns past the matrix zero-filled by the TMA unit
+constexpr int RAW_A = BK * TM * 4;
+constexpr int RAW_BYTES = BK * (TM + TN) * 4;      // 24 KB
+constexpr int NRAW = 5;
+constexpr int SMEM = NST * STAGE + NRAW * RAW_BYTES;   // 96 + 120 KB
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -100,10 +110,10 @@ __device__ __forceinline__ void mma_commit(uint64_t* b) {
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
-syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q, int64_t kchunk, const int2* __restrict__ tiles,
-                   double* __restrict__ G, int64_t ldg) {
+syrk_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t K,
+                   int64_t q, int64_t kchunk, const int2* __restrict__ tiles, double* __restrict__ G, int64_t ldg) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full[NST], empty[NST], accf[2], acce[2];
+  __shared__ __align__(8) uint64_t full[NST], empty[NST], accf[2], acce[2], rfull[NRAW], rempty[NRAW];
   __shared__ uint32_t tmem_base_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int2 tile = tiles[blockIdx.x];
@@ -121,6 +131,10 @@ syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q
       bar_init(&accf[a], 1);
       bar_init(&acce[a], 4);
     }
+    for (int r = 0; r < NRAW; ++r) {
+      bar_init(&rfull[r], 1);
+      bar_init(&rempty[r], NPROD);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 4) {
@@ -133,34 +147,43 @@ syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_s;
 
-  if (warp >= 5) {
-    // ===================== producers =====================
-    // item = (4-row K chunk kc, column c of the A|B panel): 4 coalesced 4-byte
-    // loads down the column, one 16-byte store of hi and one of lo
-    // (consecutive threads -> consecutive columns -> consecutive 16 B rows of
-    // a core matrix: conflict-free).  All loads of stage it+1 are in flight
-    // while stage it is converted (register double buffering).
+  unsigned char* raw = smem + (size_t)NST * STAGE;
+  if (warp == LOADER_WARP) {
+    // ===================== TMA loader =====================
+    if (lane == 0) {
+      for (int64_t it = 0; it < nstages; ++it) {
+        const int r = (int)(it % NRAW);
+        if (it >= NRAW) bar_wait(&rempty[r], (unsigned)(((it / NRAW) - 1) & 1));
+        const int k0 = (int)(it * BK);
+        const uint32_t dst = su32(raw + (size_t)r * RAW_BYTES), bar = su32(&rfull[r]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)RAW_BYTES)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                dst),
+            "l"(&tmA), "r"((int)i0), "r"(k0), "r"(bar)
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                dst + RAW_A),
+            "l"(&tmB), "r"((int)j0), "r"(k0), "r"(bar)
+            : "memory");
+      }
+    }
+  } else if (warp >= 5) {
+    // ===================== converters =====================
+    // item = (4-row K chunk kc, column c of the A|B panel): 4 conflict-free
+    // shared loads down the raw column, split into hi/lo, one 16-byte store of
+    // each into the K-major no-swizzle core-matrix layout (consecutive threads
+    // -> consecutive columns -> consecutive 16 B rows of a core matrix).
     constexpr int NITEM = ((BK / 4) * (TM + TN)) / (NPROD * 32);   // 6
     const int pt = tid - 5 * 32;   // 0..255
-    float cur[NITEM][4], nxt[NITEM][4];
-    auto load_stage = [&](int64_t it, float (&buf)[NITEM][4]) {
-      const int64_t k0 = it * BK;
-#pragma unroll
-      for (int u = 0; u < NITEM; ++u) {
-        const int idx = u * NPROD * 32 + pt;
-        const int kc = idx / (TM + TN);
-        const int c = idx % (TM + TN);
-        const int64_t col = c < TM ? i0 + c : j0 + (c - TM);
-        const int64_t k = k0 + 4 * kc;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) buf[u][e] = (k + e < K && col < ld) ? __ldg(A + (k + e) * ld + col) : 0.f;
-      }
-    };
-    load_stage(0, cur);
     for (int64_t it = 0; it < nstages; ++it) {
-      if (it + 1 < nstages) load_stage(it + 1, nxt);
+      const int r = (int)(it % NRAW);
       const int s = (int)(it % NST);
+      bar_wait(&rfull[r], (unsigned)((it / NRAW) & 1));
       if (it >= NST) bar_wait(&empty[s], (unsigned)(((it / NST) - 1) & 1));
+      const float* rs = reinterpret_cast<const float*>(raw + (size_t)r * RAW_BYTES);
       unsigned char* st = smem + (size_t)s * STAGE;
 #pragma unroll
       for (int u = 0; u < NITEM; ++u) {
@@ -169,11 +192,16 @@ syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q
         const int c = idx % (TM + TN);
         const bool isA = c < TM;
         const int mn = isA ? c : c - TM;
+        const float* col = isA ? rs + mn : rs + BK * TM + mn;
+        const int w = isA ? TM : TN;
+        float f[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) f[e] = col[(4 * kc + e) * w];
         uint4 hi, lo;
-        hi.x = to_tf32(cur[u][0]); lo.x = to_tf32(cur[u][0] - __uint_as_float(hi.x));
-        hi.y = to_tf32(cur[u][1]); lo.y = to_tf32(cur[u][1] - __uint_as_float(hi.y));
-        hi.z = to_tf32(cur[u][2]); lo.z = to_tf32(cur[u][2] - __uint_as_float(hi.z));
-        hi.w = to_tf32(cur[u][3]); lo.w = to_tf32(cur[u][3] - __uint_as_float(hi.w));
+        hi.x = to_tf32(f[0]); lo.x = to_tf32(f[0] - __uint_as_float(hi.x));
+        hi.y = to_tf32(f[1]); lo.y = to_tf32(f[1] - __uint_as_float(hi.y));
+        hi.z = to_tf32(f[2]); lo.z = to_tf32(f[2] - __uint_as_float(hi.z));
+        hi.w = to_tf32(f[3]); lo.w = to_tf32(f[3] - __uint_as_float(hi.w));
         unsigned char* base_hi = isA ? st : st + 2 * A_BYTES;
         const int lbo = isA ? LBO_A : LBO_B;
         const int nb = isA ? A_BYTES : B_BYTES;
@@ -183,11 +211,10 @@ syrk_tf32x3_kernel(const float* __restrict__ A, int64_t K, int64_t ld, int64_t q
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) bar_arrive(&full[s]);
-#pragma unroll
-      for (int u = 0; u < NITEM; ++u)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) cur[u][e] = nxt[u][e];
+      if (lane == 0) {
+        bar_arrive(&full[s]);
+        bar_arrive(&rempty[r]);
+      }
     }
   } else if (warp == 4) {
     // ===================== MMA issuer =====================
@@ -281,6 +308,30 @@ __global__ void upper_to_lower(double* G, int64_t q, int64_t ld) {
 
 }  // namespace syrk
 
+// 2-D tensor map over the fp32 matrix (ld columns x m rows, row stride ld*4)
+// with a BK x box_cols box, no swizzle, zero fill out of bounds.  The driver
+// entry point comes through the runtime (no libcuda link dependency).
+static CUtensorMap panel_map(const gf_matrix* A, int box_cols) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    GF_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    GF_REQUIRE(fn != nullptr && q == cudaDriverEntryPointSuccess, GF_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)A->ld, (cuuint64_t)A->m};
+  const cuuint64_t strides[1] = {(cuuint64_t)A->ld * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)syrk::BK};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, A->data, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  GF_REQUIRE(r == CUDA_SUCCESS, GF_E_CUDA, "cuTensorMapEncodeTiled failed");
+  return m;
+}
+
 // G (fp64, zeroed by the caller) += A'A for fp32 A (m x ld, columns >= n zero).
 void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st) {
   using namespace syrk;
@@ -299,8 +350,9 @@ void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st) {
   }
   const char* kc_env = getenv("GF_SYRK_KCHUNK");
   int64_t kchunk = kc_env ? std::max<int64_t>(BK, atoll(kc_env) / BK * BK) : KCHUNK_DEFAULT;
-  syrk_tf32x3_kernel<<<(unsigned)tl.size(), THREADS, SMEM, st>>>((const float*)A->data, A->m, A->ld, q, kchunk,
-                                                                 d_tiles.as<int2>(), G, ldg);
+  const CUtensorMap tmA = panel_map(A, TM), tmB = panel_map(A, TN);
+  syrk_tf32x3_kernel<<<(unsigned)tl.size(), THREADS, SMEM, st>>>(tmA, tmB, A->m, q, kchunk, d_tiles.as<int2>(), G,
+                                                                 ldg);
   GF_CHECK_LAUNCH();
   upper_to_lower<<<dim3((unsigned)ceil_div(q, 32), (unsigned)ceil_div(q, 8)), dim3(32, 8), 0, st>>>(G, q, ldg);
   GF_CHECK_LAUNCH();
