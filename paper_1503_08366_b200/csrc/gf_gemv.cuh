@@ -48,16 +48,19 @@ rowgemv_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* __res
     const V* ar = reinterpret_cast<const V*>(A + r * ld);
     T s0 = 0, s1 = 0;
     int64_t v = lane;
-    for (; v + 3 * 32 < nvec; v += 4 * 32) {
-      V a[4], b0[4], b1[4];
+    // one right-hand side: 8 row loads in flight per lane (a row of G^-1 is
+    // one warp's whole work, so the loop trip count is its latency chain)
+    constexpr int U = NRHS > 1 ? 4 : 8;
+    for (; v + (U - 1) * 32 < nvec; v += U * 32) {
+      V a[U], b0[U], b1[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < U; ++u) {
         a[u] = ld_stream(ar + v + 32 * u);
         b0[u] = ldg_vec(xv0 + v + 32 * u);
         if (NRHS > 1) b1[u] = ldg_vec(xv1 + v + 32 * u);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int i = 0; i < VN; ++i) {
           s0 = fma(vget(a[u], i), vget(b0[u], i), s0);

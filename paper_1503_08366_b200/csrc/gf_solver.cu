@@ -663,11 +663,22 @@ __device__ __forceinline__ void slab_columns(const double* __restrict__ cpart, i
   const int64_t j = c0 + lane;
   s1 = 0.0;
   s2 = 0.0;
-  if (j < n)
-    for (int64_t sl = warp; sl < slabs; sl += 8) {
-      s1 += cpart[(2 * sl) * ld + j];
-      s2 += cpart[(2 * sl + 1) * ld + j];
+  if (j < n) {   // four independent chains: 8 loads in flight per lane
+    double a1[4] = {0.0, 0.0, 0.0, 0.0}, a2[4] = {0.0, 0.0, 0.0, 0.0};
+    int64_t sl = warp;
+    for (; sl + 24 < slabs; sl += 32)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a1[u] += cpart[(2 * (sl + 8 * u)) * ld + j];
+        a2[u] += cpart[(2 * (sl + 8 * u) + 1) * ld + j];
+      }
+    for (int u = 0; sl < slabs; sl += 8, ++u) {
+      a1[u & 3] += cpart[(2 * sl) * ld + j];
+      a2[u & 3] += cpart[(2 * sl + 1) * ld + j];
     }
+    s1 = (a1[0] + a1[1]) + (a1[2] + a1[3]);
+    s2 = (a2[0] + a2[1]) + (a2[2] + a2[3]);
+  }
   part[warp][0][lane] = s1;
   part[warp][1][lane] = s2;
   __syncthreads();
@@ -762,9 +773,17 @@ zslab_tall_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ 
   double yr[kRedY + 1], xs[kRedX + 1];
   if (FROM_SLABS) block_sum_records<kRedY>(rpart, nrpart, yr, shr);
   block_sum_records<kRedX>(xpart, nxpart, xs, shx);
+  __shared__ double zs[8];
+  {
+    double z = 0.0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) z += zpart[b];
+    z = warp_sum(z);
+    if (lane == 0) zs[warp] = z;
+  }
+  __syncthreads();
   if (threadIdx.x != 0) return;
   double r2 = 0.0;
-  for (unsigned b = 0; b < gridDim.x; ++b) r2 += zpart[b];
+  for (int w = 0; w < 8; ++w) r2 += zs[w];
   ctl->ticket = 0;
   double* ys = red + 2 * ld;
   if (FROM_SLABS) y_layout(yr, ys);
@@ -975,6 +994,15 @@ static XEpi<T> make_xepi(gf_solver* s) {
   x.xk_T = s->xk_T.as<T>(); x.xh_T = s->xh_T.as<T>();
   x.n = s->n; x.alpha = s->prm.alpha; x.wide = s->tall ? 0 : 1; x.gap = s->prm.gap;
   return x;
+}
+
+// G^-1 GEMV grid: one wave of resident CTAs (the register count of the XEpi
+// instance allows 2 per SM), rows spread evenly over the warps.
+template <typename T>
+static int64_t ginv_grid(int64_t q, int sms) {
+  int b = 0;
+  GF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rowgemv_kernel<T, 1, XEpi<T>>, kRowThreads, 0));
+  return std::max<int64_t>(1, std::min<int64_t>(ceil_div(q, kRowWarps), (int64_t)sms * std::max(b, 1)));
 }
 
 template <typename T>
@@ -1211,7 +1239,7 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
   const int sms = num_sms();
   const int64_t n = s->n, m1 = std::max<int64_t>(s->m, 1), es = A->esize();
   s->grid_r = row_grid(m1, sms);
-  s->grid_s = row_grid(s->q, sms);
+  s->grid_s = s->dtype == GF_F32 ? ginv_grid<float>(s->q, sms) : ginv_grid<double>(s->q, sms);
   s->grid_z = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 2 * (int64_t)sms));
   s->grid_zt = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 32), 4 * (int64_t)sms));
   s->cplan = plan_cols(m1, s->ld, s->dtype == GF_F32 ? 4 : 2, sms);
