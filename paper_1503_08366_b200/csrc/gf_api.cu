@@ -2,6 +2,7 @@
 // lifetimes, error-code mapping, projector/setup orchestration and NCCL glue.
 
 #include <chrono>
+#include <mutex>
 #include <cstring>
 
 #include "gf_internal.h"
@@ -44,6 +45,41 @@ void allreduce_sum(gf_comm* c, double* buf, size_t count, cudaStream_t st) {
   const ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, st);
   if (r != ncclSuccess) throw_error(GF_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
 }
+
+// Grow-only per-device scratch (plain cudaMalloc, kept for the process) for
+// large setup temporaries; a ScratchLock holds the device's arena for the
+// duration of one projector build.
+struct ScratchArena {
+  std::mutex mu;
+  void* p[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t bytes[4] = {0, 0, 0, 0};
+};
+static ScratchArena& arena_for_current_device() {
+  static ScratchArena arenas[64];
+  int dev = 0;
+  GF_CUDA(cudaGetDevice(&dev));
+  return arenas[dev & 63];
+}
+struct ScratchLock {
+  ScratchArena& a;
+  std::lock_guard<std::mutex> lk;
+  ScratchLock(int count, size_t bytes) : a(arena_for_current_device()), lk(a.mu) {
+    for (int i = 0; i < count; ++i)
+      if (a.bytes[i] < bytes) {
+        if (a.p[i]) GF_CUDA(cudaFree(a.p[i]));
+        a.p[i] = nullptr;
+        a.bytes[i] = 0;
+        GF_CUDA(cudaMalloc(&a.p[i], bytes));
+        a.bytes[i] = bytes;
+      }
+  }
+  void* ptr(int i) const { return a.p[i]; }
+};
+struct DBufView {
+  void* p;
+  explicit DBufView(void* q) : p(q) {}
+  template <typename T> T* as() const { return (T*)p; }
+};
 
 // Setup phase timing (CUDA events), printed to stderr when GF_VERBOSE_SETUP=1.
 struct PhaseTimer {
@@ -171,7 +207,12 @@ static gf_projector* projector_build(gf_matrix* A, int mode, double tol, int64_t
   if (comm_active(comm)) allreduce_sum(comm, P->gram.as<double>(), (size_t)q * P->ldg, st);
   gram_finish(P->gram.as<double>(), q, P->ldg, st);
   pt.mark("gram");
-  DBuf L(gbytes), tmp(gbytes), inv(gbytes), info(sizeof(int));
+  // the three q x q fp64 temporaries come from a grow-only per-device arena:
+  // growing the stream-ordered pool by hundreds of MB mid-setup was measured
+  // to stall the host for 10-250 ms on some boxes
+  ScratchLock sl(3, gbytes);
+  DBufView L(sl.ptr(0)), tmp(sl.ptr(1)), inv(sl.ptr(2));
+  DBuf info(sizeof(int));
   GF_CUDA(cudaMemcpyAsync(L.p, P->gram.p, gbytes, cudaMemcpyDeviceToDevice, st));
   const int bad = cholesky(L.as<double>(), q, P->ldg, info.as<int>(), st);
   if (bad != 0)
@@ -240,6 +281,23 @@ int gf_init(int device) {
     GF_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t keep = UINT64_MAX;   // retain freed blocks for reuse (DBuf)
     GF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    // Pre-map part of the pool once: growing it during a setup (hundreds of
+    // MB at a time) was measured to stall the host for 10-150 ms per call.
+    // GF_POOL_RESERVE_MB (default 12288; 0 disables) is kept mapped and reused.
+    const char* env = getenv("GF_POOL_RESERVE_MB");
+    const size_t mb = env ? (size_t)atoll(env) : (size_t)12288;
+    if (mb > 0) {
+      size_t free_b = 0, total_b = 0;
+      GF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const size_t want = std::min(mb << 20, free_b / 4);
+      void* p = nullptr;
+      if (want > 0 && cudaMallocAsync(&p, want, 0) == cudaSuccess) {
+        cudaFreeAsync(p, 0);
+        GF_CUDA(cudaStreamSynchronize(0));
+      } else {
+        cudaGetLastError();
+      }
+    }
   });
 }
 

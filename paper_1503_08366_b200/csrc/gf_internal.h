@@ -1,6 +1,10 @@
 // Internal object layouts and cross-file declarations of the C-ABI library.
 #pragma once
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdint.h>
@@ -51,7 +55,12 @@ struct DBuf {
     if (p) cudaFreeAsync(p, 0);
     p = nullptr;
     bytes = b;
-    if (b) GF_CUDA(cudaMallocAsync(&p, b, 0));
+    if (b) {
+      const auto t0 = std::chrono::steady_clock::now();
+      GF_CUDA(cudaMallocAsync(&p, b, 0));
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      if (ms > 2.0 && getenv("GF_VERBOSE_SETUP")) fprintf(stderr, "[gf] slow alloc %zu bytes: %.1f ms\n", b, ms);
+    }
   }
   template <typename T> T* as() const { return (T*)p; }
 };
