@@ -139,6 +139,10 @@ int gf_matrix_download(const gf_matrix* A, double* dst, void* stream);
 /* y = A x (x: n, y: m) and y = A' x (x: m, y: n), fp64 vectors; the matvecs
  * behind residual_stop (solver.py:197-198) and the CGLS handles. */
 int gf_matvec(const gf_matrix* A, int transpose, const double* x, double* y, void* stream);
+/* y = (A o A) x and y = (A o A)' x (elementwise squares, fp64 vectors, host or
+ * device): the p = 2 |A|^p matvec handles of equilibration.py:94-125 that
+ * check_equilibrated (:227-267) and equilibration_objective (:270-287) use. */
+int gf_sq_matvec(const gf_matrix* A, int transpose, const double* x, double* y, void* stream);
 
 /* ------------------------------------------------------- equilibration -- */
 /* equilibration.py:134-197 equilibrate: regularised Sinkhorn-Knopp, p = 2.

@@ -72,6 +72,7 @@ _SIGS = {
     "gf_matrix_shape": ([_P, c_int64_p, c_int64_p, c_int64_p, c_int_p], C.c_int),
     "gf_matrix_download": ([_P, _P, _P], C.c_int),
     "gf_matvec": ([_P, C.c_int, _P, _P, _P], C.c_int),
+    "gf_sq_matvec": ([_P, C.c_int, _P, _P, _P], C.c_int),
     "gf_equilibrate": ([_P, C.c_double, C.c_double, C.c_int64, _P, _P, _P, c_int64_p, c_int_p,
                         c_double_p, _P], C.c_int),
     "gf_rescale_even": ([_P, _P, _P, _P, _P], C.c_int),

@@ -462,6 +462,22 @@ int gf_matvec(const gf_matrix* A, int transpose, const double* x, double* y, voi
   });
 }
 
+int gf_sq_matvec(const gf_matrix* A, int transpose, const double* x, double* y, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nx = transpose ? A->m : A->n, ny = transpose ? A->n : A->m;
+    DevVec xv(x, nx, st);
+    const bool yhost = ny > 0 && host_ptr(y);
+    DBuf yb;
+    double* yd = y;
+    if (yhost) { yb.alloc(ny * sizeof(double)); yd = yb.as<double>(); }
+    if (ny > 0 && nx > 0) sq_matvec(A, transpose != 0, xv.p, yd, st);
+    else if (ny > 0) GF_CUDA(cudaMemsetAsync(yd, 0, ny * sizeof(double), st));
+    if (yhost) copy_out(y, yd, ny, st);
+    GF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 int gf_equilibrate(gf_matrix* A, double gamma, double eps, int64_t max_iter, gf_comm* comm, double* d, double* e,
                    int64_t* sweeps, int* converged, double* gamma_used, void* stream) {
   return guarded([&] {

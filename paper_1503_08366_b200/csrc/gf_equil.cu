@@ -21,7 +21,7 @@ sq_row_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, int64_t n, cons
               int mode, double numer, double reg, double* __restrict__ dout, const double* __restrict__ dprev,
               const double* __restrict__ dscale, double* __restrict__ part) {
   // mode 0: Sinkhorn row update (dout = numer / (rs + reg)); mode 1: Frobenius
-  // partial sum_i dscale_i^2 * rs_i (no output vector).
+  // partial sum_i dscale_i^2 * rs_i (no output vector); mode 2: dout = rs.
   using V = typename Vec16<T>::type;
   constexpr int VN = Vec16<T>::n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -43,7 +43,10 @@ sq_row_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, int64_t n, cons
     }
     acc = warp_sum(acc);
     if (lane == 0) {
-      if (mode == 0) {
+      if (mode == 2) {          // plain weighted row sums of squares: dout = (A o A) w
+        dout[r] = acc;
+        s_rows += acc;
+      } else if (mode == 0) {
         const double dn = numer / (acc + reg);
         dout[r] = dn;
         if (dprev != nullptr) {
@@ -255,6 +258,39 @@ static void rescale_t(gf_matrix* A, double* d, double* e, gf_comm* comm, cudaStr
   scal_inplace<<<vgrid(n), 256, 0, st>>>(e, n, scal.as<double>(), 1);
   GF_CHECK_LAUNCH();
   GF_CUDA(cudaStreamSynchronize(st));
+}
+
+// y = (A o A) x (x: n) or (A o A)' x (x: m), fp64 device vectors: the p = 2
+// |A|^p handles of equilibration.py:94-125 behind check_equilibrated and
+// equilibration_objective.
+template <typename T>
+static void sq_matvec_t(const gf_matrix* A, bool transpose, const double* x, double* y, cudaStream_t st) {
+  const int sms = num_sms();
+  const int64_t m = A->m, n = A->n, ld = A->ld;
+  if (!transpose) {
+    const int64_t rgrid = row_grid(std::max<int64_t>(m, 1), sms);
+    DBuf part((size_t)rgrid * 3 * sizeof(double));
+    sq_row_kernel<T><<<(unsigned)rgrid, kRowThreads, 0, st>>>((const T*)A->data, m, ld, n, x, 2, 1.0, 0.0, y,
+                                                              nullptr, nullptr, part.as<double>());
+    GF_CHECK_LAUNCH();
+    GF_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  const ColPlan cp = plan_cols(std::max<int64_t>(m, 1), ld, Vec16<T>::n, sms);
+  DBuf cpart((size_t)cp.slabs * ld * sizeof(double)), out((size_t)ld * sizeof(double));
+  colgemv_kernel<T, 1, true><<<dim3((unsigned)cp.col_blocks, (unsigned)cp.slabs), kColThreads, 0, st>>>(
+      (const T*)A->data, m, ld, x, x, cp.rows_per_slab, cpart.as<double>(), nullptr);
+  GF_CHECK_LAUNCH();
+  colreduce_kernel<<<dim3((unsigned)ceil_div(ld, 32), 1), dim3(32, 8), 0, st>>>(cpart.as<double>(), cp.slabs, ld, 1,
+                                                                              out.as<double>(), nullptr);
+  GF_CHECK_LAUNCH();
+  GF_CUDA(cudaMemcpyAsync(y, out.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  GF_CUDA(cudaStreamSynchronize(st));
+}
+
+void sq_matvec(const gf_matrix* A, bool transpose, const double* x, double* y, cudaStream_t st) {
+  if (A->dtype == GF_F32) sq_matvec_t<float>(A, transpose, x, y, st);
+  else sq_matvec_t<double>(A, transpose, x, y, st);
 }
 
 void rescale_even(gf_matrix* A, double* d, double* e, gf_comm* comm, cudaStream_t st) {

@@ -81,6 +81,8 @@ void matrix_to_f64(const gf_matrix* M, double* dst_dev, cudaStream_t st);  // de
 void scale_matrix(gf_matrix* M, const double* d, const double* e, cudaStream_t st);
 // y = A x (x: n) / y = A' x (x: m); fp64 device vectors; ws >= matvec_ws_bytes.
 void matvec(const gf_matrix* A, bool transpose, const double* x, double* y, cudaStream_t st);
+// y = (A o A) x / (A o A)' x (equilibration diagnostics, p = 2).
+void sq_matvec(const gf_matrix* A, bool transpose, const double* x, double* y, cudaStream_t st);
 
 // ---------------------------------------------- equilibration (gf_equil) --
 struct EquilResult {
