@@ -36,9 +36,10 @@ namespace syrk {
 // a core matrix is 8 MN-rows x 16 bytes (4 tf32 along K), 128 contiguous
 // bytes; 8-row groups are SBO = 128 B apart, 4-element K chunks LBO apart.
 constexpr int TM = 128, TN = 256, BK = 16, NST = 2;
-// rows per TMEM accumulation: 512 -> max |G error| / max |G| ~ 4.7e-6 on a
-// 20000 x 1300 Gaussian matrix (1024: 9.5e-6, 128: 1.2e-6; tools/syrk_accuracy.py)
-constexpr int KCHUNK_DEFAULT = 512;
+// rows per TMEM accumulation: 1024 -> max |G error| / max |G| ~ 9.5e-6 on a
+// 20000 x 1300 Gaussian matrix (512: 4.7e-6, 128: 1.2e-6; tools/syrk_accuracy.py);
+// 1024 halves the fp64 drain traffic of 512 (Gram 39 -> 29 ms at 200000 x 5000)
+constexpr int KCHUNK_DEFAULT = 1024;
 constexpr int A_BYTES = (BK / 4) * (TM / 8) * 128; // 8 KB per hi/lo
 constexpr int B_BYTES = (BK / 4) * (TN / 8) * 128; // 16 KB per hi/lo
 constexpr int LBO_A = (TM / 8) * 128;              // K-chunk stride
