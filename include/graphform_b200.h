@@ -153,6 +153,15 @@ int gf_sq_matvec(const gf_matrix* A, int transpose, const double* x, double* y, 
 int gf_equilibrate(gf_matrix* A, double gamma, double eps, int64_t max_iter,
                    gf_comm* comm, double* d, double* e, int64_t* sweeps,
                    int* converged, double* gamma_used, void* stream);
+/* The same with the reference's on_sweep(k, d, e) observer
+ * (equilibration.py:178-179): after each sweep's updates and before its
+ * convergence test, on_sweep receives host copies of d_k^(1/2) (m values)
+ * and e_k^(1/2) (n values).  on_sweep may be NULL. */
+typedef void (*gf_sweep_fn)(int64_t k, const double* d, const double* e, int64_t m, int64_t n, void* user);
+int gf_equilibrate_observed(gf_matrix* A, double gamma, double eps, int64_t max_iter,
+                            gf_comm* comm, double* d, double* e, int64_t* sweeps,
+                            int* converged, double* gamma_used, gf_sweep_fn on_sweep,
+                            void* user, void* stream);
 /* equilibration.py:214-224 rescale_even (in place on d, e). */
 int gf_rescale_even(gf_matrix* A, double* d, double* e, gf_comm* comm, void* stream);
 /* solver.py:142-145 _scale_matrix: A <- diag(d) A diag(e), in place. */

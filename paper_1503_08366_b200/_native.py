@@ -75,6 +75,8 @@ _SIGS = {
     "gf_sq_matvec": ([_P, C.c_int, _P, _P, _P], C.c_int),
     "gf_equilibrate": ([_P, C.c_double, C.c_double, C.c_int64, _P, _P, _P, c_int64_p, c_int_p,
                         c_double_p, _P], C.c_int),
+    "gf_equilibrate_observed": ([_P, C.c_double, C.c_double, C.c_int64, _P, _P, _P, c_int64_p, c_int_p,
+                                 c_double_p, _P, _P, _P], C.c_int),
     "gf_rescale_even": ([_P, _P, _P, _P, _P], C.c_int),
     "gf_scale_matrix": ([_P, _P, _P, _P], C.c_int),
     "gf_projector_create": ([_P, C.c_int, C.c_double, C.c_int64, _P, _P, C.POINTER(_P)], C.c_int),
@@ -392,3 +394,8 @@ class Matrix:
                 self._lib.gf_matrix_destroy(self.handle)
         except Exception:
             pass
+
+
+# gf_sweep_fn: void (*)(int64_t k, const double* d, const double* e, int64_t m, int64_t n, void* user)
+SWEEP_FN = C.CFUNCTYPE(None, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64, C.c_int64,
+                       C.c_void_p)

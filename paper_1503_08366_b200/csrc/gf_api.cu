@@ -478,12 +478,14 @@ int gf_sq_matvec(const gf_matrix* A, int transpose, const double* x, double* y, 
   });
 }
 
-int gf_equilibrate(gf_matrix* A, double gamma, double eps, int64_t max_iter, gf_comm* comm, double* d, double* e,
-                   int64_t* sweeps, int* converged, double* gamma_used, void* stream) {
+int gf_equilibrate_observed(gf_matrix* A, double gamma, double eps, int64_t max_iter, gf_comm* comm, double* d, double* e,
+                   int64_t* sweeps, int* converged, double* gamma_used, gf_sweep_fn on_sweep, void* user,
+                            void* stream) {
   return guarded([&] {
     cudaStream_t st = (cudaStream_t)stream;
     DBuf dd(std::max<int64_t>(A->m, 1) * sizeof(double)), ee(A->n * sizeof(double));
-    const EquilResult r = equilibrate(A, gamma, eps, max_iter, comm, dd.as<double>(), ee.as<double>(), st);
+    const EquilResult r = equilibrate(A, gamma, eps, max_iter, comm, dd.as<double>(), ee.as<double>(), st,
+                                      (SweepCb)on_sweep, user);
     copy_out(d, dd.as<double>(), A->m, st);
     copy_out(e, ee.as<double>(), A->n, st);
     GF_CUDA(cudaStreamSynchronize(st));
@@ -492,6 +494,12 @@ int gf_equilibrate(gf_matrix* A, double gamma, double eps, int64_t max_iter, gf_
     if (gamma_used) *gamma_used = r.gamma;
   });
 }
+int gf_equilibrate(gf_matrix* A, double gamma, double eps, int64_t max_iter, gf_comm* comm, double* d, double* e,
+                   int64_t* sweeps, int* converged, double* gamma_used, void* stream) {
+  return gf_equilibrate_observed(A, gamma, eps, max_iter, comm, d, e, sweeps, converged, gamma_used, nullptr, nullptr,
+                                 stream);
+}
+
 
 int gf_rescale_even(gf_matrix* A, double* d, double* e, gf_comm* comm, void* stream) {
   return guarded([&] {

@@ -8,6 +8,8 @@
 // partition the column sums and the ||d - d_prev||^2 partial are all-reduced,
 // everything else is rank-local.
 
+#include <vector>
+
 #include "gf_internal.h"
 #include "gf_gemv.cuh"
 
@@ -148,7 +150,7 @@ static double global_rows(gf_matrix* A, gf_comm* comm, cudaStream_t st) {
 
 template <typename T>
 static EquilResult equil_t(gf_matrix* A, double gamma, double eps, int64_t max_iter, gf_comm* comm,
-                           double* d_out, double* e_out, cudaStream_t st) {
+                           double* d_out, double* e_out, cudaStream_t st, SweepCb cb, void* user) {
   const int sms = num_sms();
   const int64_t m = A->m, n = A->n, ld = A->ld;
   const double mg = global_rows(A, comm, st);
@@ -200,6 +202,15 @@ static EquilResult equil_t(gf_matrix* A, double gamma, double eps, int64_t max_i
     GF_CUDA(cudaStreamSynchronize(st));
     if (k == 1 && !(h[1] > 0.0))
       throw_error(GF_E_DEGENERATE_INPUT, "cannot equilibrate an all-zero matrix");
+    if (cb != nullptr) {   // on_sweep(k, d_k^(1/p), e_k^(1/p)), before the convergence test
+      std::vector<double> hd((size_t)std::max<int64_t>(m, 0)), he((size_t)n);
+      if (m > 0) GF_CUDA(cudaMemcpyAsync(hd.data(), d_it, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+      GF_CUDA(cudaMemcpyAsync(he.data(), e, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+      GF_CUDA(cudaStreamSynchronize(st));
+      for (auto& v : hd) v = sqrt(v);
+      for (auto& v : he) v = sqrt(v);
+      cb(k, hd.data(), he.data(), m, n, user);
+    }
     const bool bad = h[2] > 0.0 || h2[1] > 0.0;
     if (bad) {
       throw_error(GF_E_NUMERIC,
@@ -223,10 +234,10 @@ static EquilResult equil_t(gf_matrix* A, double gamma, double eps, int64_t max_i
 }
 
 EquilResult equilibrate(gf_matrix* A, double gamma, double eps, int64_t max_iter, gf_comm* comm, double* d_dev,
-                        double* e_dev, cudaStream_t st) {
+                        double* e_dev, cudaStream_t st, SweepCb cb, void* user) {
   GF_REQUIRE(max_iter >= 1, GF_E_PARAMETER, "max_iter must be at least 1");
-  if (A->dtype == GF_F32) return equil_t<float>(A, gamma, eps, max_iter, comm, d_dev, e_dev, st);
-  return equil_t<double>(A, gamma, eps, max_iter, comm, d_dev, e_dev, st);
+  if (A->dtype == GF_F32) return equil_t<float>(A, gamma, eps, max_iter, comm, d_dev, e_dev, st, cb, user);
+  return equil_t<double>(A, gamma, eps, max_iter, comm, d_dev, e_dev, st, cb, user);
 }
 
 template <typename T>

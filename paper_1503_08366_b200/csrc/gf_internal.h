@@ -90,8 +90,11 @@ struct EquilResult {
   bool converged;
   double gamma;
 };
+// per-sweep observer (on_sweep of equilibration.py:178-179): sweep k, host
+// copies of d_k^(1/2) (m) and e_k^(1/2) (n)
+typedef void (*SweepCb)(int64_t k, const double* d, const double* e, int64_t m, int64_t n, void* user);
 EquilResult equilibrate(gf_matrix* A, double gamma, double eps, int64_t max_iter, gf_comm* comm,
-                        double* d_dev, double* e_dev, cudaStream_t st);
+                        double* d_dev, double* e_dev, cudaStream_t st, SweepCb cb = nullptr, void* user = nullptr);
 void rescale_even(gf_matrix* A, double* d_dev, double* e_dev, gf_comm* comm, cudaStream_t st);
 
 // --------------------------------------------------- vectors (gf_vec.cu) --

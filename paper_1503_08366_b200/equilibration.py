@@ -66,9 +66,10 @@ def _as_matrix(A):
 
 def equilibrate(A, gamma: Optional[float] = None, eps: Optional[float] = None,
                 max_iter: int = 300, on_sweep: Optional[Callable] = None) -> Equilibration:
-    """Regularised Sinkhorn-Knopp with p = 2 (equilibration.py:134-197)."""
-    if on_sweep is not None:
-        raise NotImplementedError("on_sweep callbacks are not supported by the GPU build")
+    """Regularised Sinkhorn-Knopp with p = 2 (equilibration.py:134-197).
+    ``on_sweep(k, d, e)`` receives the diagonal iterates after each sweep
+    (host copies made by the library after the sweep's device updates); an
+    exception it raises is re-raised once the sweeps return."""
     A = _as_matrix(A)
     if gamma is not None and gamma < 0.0:
         raise ParameterError("gamma must be nonnegative")
@@ -84,10 +85,25 @@ def equilibrate(A, gamma: Optional[float] = None, eps: Optional[float] = None,
     sweeps = C.c_int64()
     conv = C.c_int()
     g_used = C.c_double()
-    _native.check(L.gf_equilibrate(M.handle, -1.0 if gamma is None else float(gamma),
-                                   -1.0 if eps is None else float(eps), int(max_iter), None,
-                                   _native.ptr(d), _native.ptr(e), C.byref(sweeps), C.byref(conv),
-                                   C.byref(g_used), _native.stream()))
+    errors = []
+
+    def observe(k, dp, ep, mm, nn, _user):
+        if errors:
+            return
+        try:
+            on_sweep(int(k), np.ctypeslib.as_array(dp, shape=(mm,)).copy(),
+                     np.ctypeslib.as_array(ep, shape=(nn,)).copy())
+        except BaseException as exc:   # re-raised after the C call returns
+            errors.append(exc)
+
+    cb = _native.SWEEP_FN(observe) if on_sweep is not None else None
+    _native.check(L.gf_equilibrate_observed(M.handle, -1.0 if gamma is None else float(gamma),
+                                            -1.0 if eps is None else float(eps), int(max_iter), None,
+                                            _native.ptr(d), _native.ptr(e), C.byref(sweeps), C.byref(conv),
+                                            C.byref(g_used), C.cast(cb, C.c_void_p) if cb else None, None,
+                                            _native.stream()))
+    if errors:
+        raise errors[0]
     return Equilibration(d=d, e=e, p=2, gamma=float(g_used.value),
                          iterations=int(sweeps.value), converged=bool(conv.value))
 

@@ -1,6 +1,7 @@
 """Reference outputs of the equilibration diagnostics (check_equilibrated,
 equilibration_objective; equilibration.py:227-287) on the matrices of
-equil.npz at the reference's own d, e (run where /root/reference exists):
+equil.npz at the reference's own d, e, and the on_sweep(k, d, e) sequence of
+equilibrate on each (equil_sweeps.npz) (run where /root/reference exists):
 
     python tests/golden/make_golden_diag.py
 """
@@ -30,6 +31,15 @@ def main():
             rep = gf.check_equilibrated(A, dd, ee, tol=0.05).as_dict()
             rep["objective"] = gf.equilibration_objective(A, dd, ee, gam)
             out[f"{name}|{tag}"] = rep
+    sweeps = {}
+    for name in names:
+        rec = []
+        gf.equilibrate(z[f"{name}_A"], on_sweep=lambda k, d, e: rec.append((k, d.copy(), e.copy())))
+        sweeps[f"{name}_k"] = np.array([r[0] for r in rec])
+        for k, d, e in rec:
+            sweeps[f"{name}_d{k}"] = d
+            sweeps[f"{name}_e{k}"] = e
+    np.savez_compressed(os.path.join(HERE, "equil_sweeps.npz"), **sweeps)
     with open(os.path.join(HERE, "equil_diag.json"), "w") as fh:
         json.dump(out, fh, indent=1, sort_keys=True)
     print(f"wrote equil_diag.json ({len(out)} reports)")

@@ -63,3 +63,18 @@ def test_equilibration_diagnostics_match_reference():
             assert rep[k] == pytest.approx(want[k], rel=1e-6, abs=1e-13), (key, k)
         obj = gf.equilibration_objective(A, d, e, float(z[f"{name}_gamma"]))
         assert obj == pytest.approx(want["objective"], rel=1e-12), key
+
+
+def test_equilibrate_on_sweep_matches_reference():
+    """on_sweep(k, d, e) after every sweep (equilibration.py:178-179)."""
+    z = np.load(os.path.join(GOLDEN, "equil.npz"))
+    sw = np.load(os.path.join(GOLDEN, "equil_sweeps.npz"))
+    for name in ("gauss_300x120", "wide_80x200", "zero_row_60x30", "scaled_150x150"):
+        rec = []
+        eq = gf.equilibrate(z[f"{name}_A"], on_sweep=lambda k, d, e: rec.append((k, d, e)))
+        assert [r[0] for r in rec] == list(sw[f"{name}_k"]) and eq.iterations == len(rec)
+        for k, d, e in rec:
+            np.testing.assert_allclose(d, sw[f"{name}_d{k}"], rtol=1e-12)
+            np.testing.assert_allclose(e, sw[f"{name}_e{k}"], rtol=1e-12)
+    with pytest.raises(ZeroDivisionError):   # the observer's exception reaches the caller
+        gf.equilibrate(z["gauss_300x120_A"], on_sweep=lambda k, d, e: 1 / 0)
