@@ -288,7 +288,6 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
   __shared__ T red_s[NE][kFusedWarps][K];
   __shared__ T w_s[NE][TR][2];
 
-  if (!epi.active()) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t nvec = ld / VN;
   const unsigned rb = (unsigned)(ld * sizeof(T));
@@ -314,10 +313,25 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
 
   if (warp == kProdWarp) {
     // ===================== producer warp =====================
+    // A_hat does not depend on the previous kernel: the first ring fill is
+    // issued before the programmatic-dependency wait (overlapping the
+    // predecessor's tail); if the solve has ended meanwhile the copies are
+    // drained before the CTA exits.
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      int slot = 0;
-      for (int j = 0; j < nr; ++j) {
+      const int pre = min(nslot, nr);
+      for (int j = 0; j < pre; ++j) {
+        mbar_arrive_expect_tx(&full[j], rb);
+        bulk_g2s(smem_raw + j * rb, A + (r0 + j) * ld, rb, &full[j], pol);
+      }
+      pdl_wait();
+      pdl_trigger();
+      if (!epi.active()) {
+        for (int j = 0; j < pre; ++j) mbar_wait(&full[j], 0u);
+        return;
+      }
+      int slot = pre == nslot ? 0 : pre;
+      for (int j = pre; j < nr; ++j) {
 #ifdef GF_FUSED_TRACE
         long long c0 = clock64();
 #endif
@@ -333,6 +347,8 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
     return;
   }
 
+  pdl_wait();
+  if (!epi.active()) return;
   if (warp >= kEpiWarp && warp < kEpiWarp + NE) {
     // ===================== epilogue warps =====================
     const int par = warp - kEpiWarp;   // this warp's groups and buffer

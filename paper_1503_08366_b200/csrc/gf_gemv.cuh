@@ -32,6 +32,8 @@ template <typename T, int NRHS, class Epi>
 __global__ void __launch_bounds__(kRowThreads)
 rowgemv_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* __restrict__ x0,
                const T* __restrict__ x1, Epi epi, double* __restrict__ part) {
+  pdl_wait();
+  pdl_trigger();
   if (!epi.active()) return;
   using V = typename Vec16<T>::type;
   constexpr int VN = Vec16<T>::n;

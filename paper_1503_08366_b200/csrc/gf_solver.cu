@@ -734,6 +734,8 @@ zslab_tall_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ 
                   const double* __restrict__ e, const double* __restrict__ muh2, T* __restrict__ rhs_T,
                   double* __restrict__ zpart, const double* __restrict__ xpart, int64_t nxpart,
                   double* __restrict__ hist, double* __restrict__ red) {
+  pdl_wait();
+  pdl_trigger();
   if (ctl->status != GF_STATUS_RUNNING) return;
   __shared__ double part[8][2][33];
   __shared__ double shr[8][kRedY + 1];
@@ -922,6 +924,34 @@ static YEpi<T> make_yepi(gf_solver* s) {
   return y;
 }
 
+// Launch with the programmatic-stream-serialization attribute when `pdl`
+// (the three kernels of a tall iteration: each waits on its predecessor with
+// pdl_wait(), so launch processing and the fused kernel's first ring fill
+// overlap the previous kernel's tail).
+template <typename... KArgs, typename... Args>
+static void launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl ? at : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  GF_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
+static bool use_pdl(const gf_solver* s) {
+  static const bool off = [] {
+    const char* e = getenv("GF_DISABLE_PDL");
+    return e && e[0] == '1';
+  }();
+  return !off && !s->profile && !comm_active(s->S->comm);
+}
+
 // attr_only: set the dynamic shared-memory limit of the instance (at create)
 template <typename T, int NV, int TR, int CW>
 static void fused_go(gf_solver* s, cudaStream_t st, bool attr_only) {
@@ -931,9 +961,9 @@ static void fused_go(gf_solver* s, cudaStream_t st, bool attr_only) {
     GF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
     return;
   }
-  kern<<<p.grid, fused_threads(CW), p.smem, st>>>((const T*)s->S->A->data, s->m, s->ld, s->xk_T.as<T>(),
-                                                  s->xh_T.as<T>(), make_yepi<T>(s), p.nslot,
-                                                  s->rpart.as<double>(), s->cpart.as<double>());
+  launch_k(use_pdl(s), kern, dim3(p.grid), dim3(fused_threads(CW)), p.smem, st, (const T*)s->S->A->data, s->m,
+           s->ld, (const T*)s->xk_T.as<T>(), (const T*)s->xh_T.as<T>(), make_yepi<T>(s), p.nslot,
+           s->rpart.as<double>(), s->cpart.as<double>());
   GF_CHECK_LAUNCH();
 }
 
@@ -1034,8 +1064,9 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
     s->launches += 1;
   } else if (k > 0) {  // S(k-1): x+ = Ginv rhs and the x side of iteration k
     s->mark(0, st, true);
-    rowgemv_kernel<T, 1, XEpi<T>><<<(unsigned)s->grid_s, kRowThreads, 0, st>>>(
-        P->ginv.as<T>(), s->q, s->ldq, s->rhs_T.as<T>(), s->rhs_T.as<T>(), make_xepi<T>(s), s->xpart.as<double>());
+    launch_k(use_pdl(s), rowgemv_kernel<T, 1, XEpi<T>>, dim3((unsigned)s->grid_s), dim3(kRowThreads), 0, st,
+             (const T*)P->ginv.as<T>(), s->q, s->ldq, (const T*)s->rhs_T.as<T>(), (const T*)s->rhs_T.as<T>(),
+             make_xepi<T>(s), s->xpart.as<double>());
     GF_CHECK_LAUNCH();
     s->mark(0, st, false);
     s->launches += 1;
@@ -1067,10 +1098,11 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
     }
     if (!comm_active(s->S->comm)) {   // Z(k) in one launch: slab + y reduce + controller
       s->mark(5, st, true);
-      zslab_tall_kernel<T, true><<<(unsigned)s->grid_zt, 256, 0, st>>>(
-          ctl, s->prm, s->cpart.as<double>(), slabs, s->ld, s->n, s->rpart.as<double>(), nrpart,
-          s->cx.as<double>(), s->S->e.as<double>(), s->muh2.as<double>(), s->rhs_T.as<T>(), s->zpart.as<double>(),
-          s->xpart.as<double>(), s->grid_s, s->hist.as<double>(), s->red.as<double>());
+      launch_k(use_pdl(s), zslab_tall_kernel<T, true>, dim3((unsigned)s->grid_zt), dim3(256), 0, st, ctl, s->prm,
+               (const double*)s->cpart.as<double>(), slabs, s->ld, s->n, (const double*)s->rpart.as<double>(),
+               nrpart, (const double*)s->cx.as<double>(), (const double*)s->S->e.as<double>(),
+               (const double*)s->muh2.as<double>(), s->rhs_T.as<T>(), s->zpart.as<double>(),
+               (const double*)s->xpart.as<double>(), s->grid_s, s->hist.as<double>(), s->red.as<double>());
       GF_CHECK_LAUNCH();
       s->mark(5, st, false);
       s->launches += 1;
