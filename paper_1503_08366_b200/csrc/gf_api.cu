@@ -412,7 +412,10 @@ int gf_matrix_create(int dtype, int64_t m, int64_t n, const void* src, int src_d
     M->n = n;
     M->ld = padded_ld(n, dtype);
     const size_t bytes = (size_t)std::max<int64_t>(m, 1) * M->ld * M->esize();
-    GF_CUDA(cudaMalloc(&M->data, bytes));
+    // from the stream-ordered pool (retained across solves): a plain
+    // cudaMalloc/cudaFree of gigabytes maps/unmaps memory and was measured to
+    // stall solve() teardown for up to 0.7 s
+    GF_CUDA(cudaMallocAsync(&M->data, bytes, 0));
     if (m > 0) matrix_upload(M.get(), src, src_dtype, src_ld, (cudaStream_t)stream);
     GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     *out = M.release();
@@ -422,7 +425,7 @@ int gf_matrix_create(int dtype, int64_t m, int64_t n, const void* src, int src_d
 int gf_matrix_destroy(gf_matrix* A) {
   return guarded([&] {
     if (A == nullptr) return;
-    if (A->data) cudaFree(A->data);
+    if (A->data) cudaFreeAsync(A->data, 0);
     delete A;
   });
 }

@@ -186,8 +186,10 @@ inline ColPlan plan_cols(int64_t rows, int64_t ld, int vn, int sms) {
   ColPlan p;
   const int64_t nvec = ld / vn;
   p.col_blocks = ceil_div(nvec, kColThreads);
-  // about 2 waves of CTAs, and at least 64 rows per slab
-  int64_t want = std::max<int64_t>(1, (int64_t)2 * sms / p.col_blocks);
+  // about 4 CTAs per SM (what the registers allow: 1024 threads x 4 rows of
+  // 16-byte loads in flight, ~64 KB per SM -- with 2 per SM the pass ran at
+  // 2.8 TB/s), and at least 64 rows per slab
+  int64_t want = std::max<int64_t>(1, (int64_t)4 * sms / p.col_blocks);
   want = std::min<int64_t>(want, std::max<int64_t>(1, rows / 64));
   want = std::min<int64_t>(want, 4096);
   p.rows_per_slab = ceil_div(std::max<int64_t>(rows, 1), want);

@@ -25,6 +25,8 @@
 // The controller lives on the device, so a chunk of iterations runs without a
 // host round trip; kernels of iterations after termination return at entry.
 
+#include <mutex>
+
 #include "gf_internal.h"
 #include "gf_gemv.cuh"
 #include "gf_fused.cuh"
@@ -842,6 +844,31 @@ __global__ void div_into(const double* __restrict__ src, int64_t n, double rho, 
 
 }  // namespace gf
 
+// Pinned controller read-back buffers (2 x Ctl per solver) come from a
+// process-wide free list: cudaMallocHost / cudaFreeHost per solver cost
+// milliseconds and synchronise the device.
+namespace gf {
+static std::mutex g_pinned_mu;
+static std::vector<Ctl*> g_pinned_free;
+static Ctl* pinned_acquire() {
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    if (!g_pinned_free.empty()) {
+      Ctl* p = g_pinned_free.back();
+      g_pinned_free.pop_back();
+      return p;
+    }
+  }
+  Ctl* p = nullptr;
+  GF_CUDA(cudaMallocHost(&p, 2 * sizeof(Ctl)));
+  return p;
+}
+static void pinned_release(Ctl* p) {
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  g_pinned_free.push_back(p);
+}
+}  // namespace gf
+
 // ============================================================== driver ====
 using namespace gf;
 
@@ -878,7 +905,7 @@ struct gf_solver {
   double kms[8] = {0};
   int64_t kcount[8] = {0};
   ~gf_solver() {
-    if (pinned) cudaFreeHost(pinned);
+    if (pinned) pinned_release(pinned);
     if (ev_a) cudaEventDestroy(ev_a);
     if (ev_b) cudaEventDestroy(ev_b);
     for (auto e : ev_done)
@@ -1313,7 +1340,7 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
   c.rho = st_in->rho0; c.rho_prev = st_in->rho0; c.ratio = 1.0; c.final_rho = st_in->rho0;
   c.r_pri = INFINITY; c.r_dual = INFINITY;
   GF_CUDA(cudaMemcpyAsync(s->ctl.p, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
-  GF_CUDA(cudaMallocHost(&s->pinned, 2 * sizeof(Ctl)));
+  s->pinned = pinned_acquire();
   GF_CUDA(cudaEventCreateWithFlags(&s->ev_done[0], cudaEventDisableTiming));
   GF_CUDA(cudaEventCreateWithFlags(&s->ev_done[1], cudaEventDisableTiming));
   GF_CUDA(cudaEventCreate(&s->ev_a));

@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 import time
+import weakref
 from dataclasses import dataclass
 from typing import Callable, Optional
 
@@ -145,8 +146,21 @@ class Setup:
         mh = C.c_void_p()
         _native.check(L.gf_setup_matrix(handle, C.byref(mh)))
         self._mview = _MatrixView(mh, m, n)
-        self.projector = ProjectorCache(ph, self._mview, mode, m, n, tol, max_inner, owner=self)
+        # the projector view holds this Setup (its owner); the Setup keeps only a
+        # weak reference back, so dropping the Setup frees the device memory at
+        # once instead of at the next cyclic garbage collection
+        self._proj_args = (ph, mode, m, n, tol, max_inner)
+        self._proj_ref = None
         self._A_hat = None
+
+    @property
+    def projector(self) -> ProjectorCache:
+        p = self._proj_ref() if self._proj_ref is not None else None
+        if p is None:
+            ph, mode, m, n, tol, max_inner = self._proj_args
+            p = ProjectorCache(ph, self._mview, mode, m, n, tol, max_inner, owner=self)
+            self._proj_ref = weakref.ref(p)
+        return p
 
     @property
     def A_hat(self):
