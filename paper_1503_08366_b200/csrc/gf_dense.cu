@@ -16,6 +16,7 @@
 // O(m q^2) Gram.  The Gram itself reads the working-dtype matrix and
 // accumulates in fp64.
 
+#include <type_traits>
 #include <vector>
 
 #include "gf_internal.h"
@@ -99,11 +100,136 @@ __global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t
   }
 }
 
+// ------------------------------------------------- fp64 tensor-core GEMM --
+// The same contract for fp64 operands on B200's fp64 tensor cores
+// (mma.sync m8n8k4 f64 -> DMMA): 128 x 64 output tile per 256-thread CTA
+// (8 warps as 4 x 2, 32 x 32 per warp = 4 x 4 MMA tiles, 32 fp64
+// accumulators per thread), 16-deep K slices staged in shared memory with a
+// register prefetch of the next slice.  Shared rows are padded to 8 mod 16
+// doubles so each fragment load (4 k-rows x 8 m/n-columns per warp) fills
+// the 16 double-wide banks exactly twice.  Used for the fp64 Gram, the
+// Cholesky trailing updates, TRTRI and W'W.
+constexpr int TBM = 128, TBN = 64, TBK = 16, TPA = TBM + 8, TPB = TBN + 8;
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <bool AT, bool BT>
+__global__ void __launch_bounds__(256) dgemm_tc_kernel(int64_t M, int64_t N, int64_t K, double alpha,
+                                                       const double* __restrict__ A, int64_t lda, int64_t sA,
+                                                       const double* __restrict__ B, int64_t ldb, int64_t sB,
+                                                       double beta, double* __restrict__ C, int64_t ldc,
+                                                       int64_t sC, int lower_only) {
+  const int64_t i0 = (int64_t)blockIdx.y * TBM, j0 = (int64_t)blockIdx.x * TBN;
+  if (lower_only && j0 > i0 + TBM - 1) return;
+  A += blockIdx.z * sA;
+  B += blockIdx.z * sB;
+  C += blockIdx.z * sC;
+  __shared__ __align__(16) double As[TBK][TPA];
+  __shared__ __align__(16) double Bs[TBK][TPB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2;
+  double ra[8], rb[4];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int idx = s * 256 + tid;
+      int ii, kk;
+      if (AT) { kk = idx >> 7; ii = idx & 127; } else { kk = idx & 15; ii = idx >> 4; }
+      const int64_t gi = i0 + ii, gk = k0 + kk;
+      ra[s] = (gi < M && gk < K) ? (AT ? A[gk * lda + gi] : A[gi * lda + gk]) : 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int idx = s * 256 + tid;
+      int nn, kk;
+      if (BT) { kk = idx & 15; nn = idx >> 4; } else { kk = idx >> 6; nn = idx & 63; }
+      const int64_t gj = j0 + nn, gk = k0 + kk;
+      rb[s] = (gj < N && gk < K) ? (BT ? B[gj * ldb + gk] : B[gk * ldb + gj]) : 0.0;
+    }
+  };
+  auto store = [&]() {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int idx = s * 256 + tid;
+      int ii, kk;
+      if (AT) { kk = idx >> 7; ii = idx & 127; } else { kk = idx & 15; ii = idx >> 4; }
+      As[kk][ii] = ra[s];
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int idx = s * 256 + tid;
+      int nn, kk;
+      if (BT) { kk = idx & 15; nn = idx >> 4; } else { kk = idx >> 6; nn = idx & 63; }
+      Bs[kk][nn] = rb[s];
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int fk = lane & 3, fr = lane >> 2;   // fragment k row, m/n column
+  load(0);
+  for (int64_t k0 = 0; k0 < K; k0 += TBK) {
+    store();
+    __syncthreads();
+    if (k0 + TBK < K) load(k0 + TBK);   // next slice in flight during the MMAs
+#pragma unroll
+    for (int ks = 0; ks < TBK / 4; ++ks) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        fa[t] = As[ks * 4 + fk][wm * 32 + t * 8 + fr];
+        fb[t] = Bs[ks * 4 + fk][wn * 32 + t * 8 + fr];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int64_t gi = i0 + wm * 32 + a * 8 + fr;
+    if (gi >= M) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gj = j0 + wn * 32 + b * 8 + fk * 2 + h;
+        if (gj >= N) continue;
+        double* c = C + gi * ldc + gj;
+        *c = beta == 0.0 ? alpha * acc[a][b][h] : alpha * acc[a][b][h] + beta * *c;
+      }
+  }
+}
+
 template <typename TA, typename TB, bool AT, bool BT>
 static void gemm(int64_t M, int64_t N, int64_t K, double alpha, const TA* A, int64_t lda,
                  const TB* B, int64_t ldb, double beta, double* C, int64_t ldc, bool lower,
                  cudaStream_t st, int batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0) {
   if (M <= 0 || N <= 0) return;
+  if constexpr (std::is_same<TA, double>::value && std::is_same<TB, double>::value) {
+    static const bool simt = [] {
+      const char* e = getenv("GF_DGEMM_SIMT");
+      return e && e[0] == '1';
+    }();
+    // fp64 tensor cores (DMMA) for long reductions; short-K updates (the
+    // 128-deep Cholesky trailing updates) are faster on the SIMT tile, whose
+    // smaller CTAs fill the machine better (measured at q = 5000 and 20000)
+    if (!simt && K >= 512) {
+      dim3 grid((unsigned)ceil_div(N, TBN), (unsigned)ceil_div(M, TBM), (unsigned)batch);
+      dgemm_tc_kernel<AT, BT><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC,
+                                                    lower ? 1 : 0);
+      GF_CHECK_LAUNCH();
+      return;
+    }
+  }
   dim3 grid((unsigned)ceil_div(N, GB), (unsigned)ceil_div(M, GB), (unsigned)batch);
   gemm_kernel<TA, TB, AT, BT><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, sA, B, ldb, sB,
                                                     beta, C, ldc, sC, lower ? 1 : 0);

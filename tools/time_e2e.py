@@ -16,7 +16,7 @@ for rep in range(4):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     M = _native.Matrix(A_pin, _native.GF_F32)
     torch.cuda.synchronize(); t1 = time.perf_counter()
-    M.release(); del M
+    del M   # (release() would hand ownership away and leak the 4 GB copy)
     torch.cuda.synchronize(); t2 = time.perf_counter()
     res = gf.solve(p)
     torch.cuda.synchronize(); t3 = time.perf_counter()
