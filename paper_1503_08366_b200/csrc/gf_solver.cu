@@ -30,6 +30,7 @@
 #include "gf_internal.h"
 #include "gf_gemv.cuh"
 #include "gf_fused.cuh"
+#include "gf_ring.cuh"
 
 namespace gf {
 
@@ -890,6 +891,7 @@ struct gf_solver {
   int64_t grid_r = 1, grid_s = 1, grid_z = 1, grid_zt = 1;
   ColPlan cplan;
   FusedPlan fplan;
+  RingPlan rplan;     // S step on the TMA row ring (tall, direct)
   int warm_x = 0;
   int64_t next_step = 0;  // step k = [S(k-1)], R(k), C(k), Z(k)
   Ctl host{};
@@ -1035,6 +1037,46 @@ static void fused_dispatch(gf_solver* s, cudaStream_t st, bool attr_only) {
 }
 
 template <typename T>
+static XEpi<T> make_xepi(gf_solver* s);
+
+template <typename T, int NV, int CW>
+static void ring_go(gf_solver* s, cudaStream_t st, bool attr_only) {
+  const RingPlan& p = s->rplan;
+  auto kern = ring_gemv_kernel<T, NV, CW, XEpi<T>>;
+  if (attr_only) {
+    GF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    return;
+  }
+  launch_k(use_pdl(s), kern, dim3(p.grid), dim3((CW + 2) * 32), p.smem, st, (const T*)s->S->P->ginv.as<T>(), s->q,
+           s->ldq, (const T*)s->rhs_T.as<T>(), make_xepi<T>(s), p.nslot, s->xpart.as<double>(), s->grid_s);
+}
+
+template <typename T>
+static void ring_dispatch(gf_solver* s, cudaStream_t st, bool attr_only) {
+  const int nv = s->rplan.nv;
+  switch (s->rplan.cw) {
+    case 8:
+      switch (nv) {
+        case 1: ring_go<T, 1, 8>(s, st, attr_only); break;
+        case 2: ring_go<T, 2, 8>(s, st, attr_only); break;
+        case 3: ring_go<T, 3, 8>(s, st, attr_only); break;
+        case 4: ring_go<T, 4, 8>(s, st, attr_only); break;
+        default: ring_go<T, 5, 8>(s, st, attr_only); break;
+      }
+      return;
+    case 12:
+      if (nv == 4) ring_go<T, 4, 12>(s, st, attr_only); else ring_go<T, 5, 12>(s, st, attr_only);
+      return;
+    case 16:
+      ring_go<T, 4, 16>(s, st, attr_only);
+      return;
+    default:
+      ring_go<T, 4, 20>(s, st, attr_only);
+      return;
+  }
+}
+
+template <typename T>
 static void fused_prepare(gf_solver* s) { fused_dispatch<T>(s, nullptr, true); }
 
 template <typename T>
@@ -1091,6 +1133,8 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
     s->launches += 1;
   } else if (k > 0) {  // S(k-1): x+ = Ginv rhs and the x side of iteration k
     s->mark(0, st, true);
+    if (s->rplan.ok) ring_dispatch<T>(s, st, false);
+    else
     launch_k(use_pdl(s), rowgemv_kernel<T, 1, XEpi<T>>, dim3((unsigned)s->grid_s), dim3(kRowThreads), 0, st,
              (const T*)P->ginv.as<T>(), s->q, s->ldq, (const T*)s->rhs_T.as<T>(), (const T*)s->rhs_T.as<T>(),
              make_xepi<T>(s), s->xpart.as<double>());
@@ -1311,6 +1355,15 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
     int dev = 0, optin = 0;
     GF_CUDA(cudaGetDevice(&dev));
     GF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    {   // (the indirect projector has no G^-1: ldq is 0)
+      const char* renv = getenv("GF_DISABLE_RING");
+      if (!(renv && renv[0] == '1') && s->tall && !s->indirect && s->ldq > 0)
+        s->rplan = plan_ring(s->q, s->ldq, (int)es, sms, (size_t)optin, s->grid_s);
+    }
+    if (s->rplan.ok) {
+      if (s->dtype == GF_F32) ring_dispatch<float>(s.get(), nullptr, true);
+      else ring_dispatch<double>(s.get(), nullptr, true);
+    }
     s->fplan = plan_fused(s->m, s->ld, (int)es, sms, (size_t)optin);
     const char* env = getenv("GF_DISABLE_FUSED");
     if ((env && env[0] == '1') || !s->tall) s->fplan.ok = false;
