@@ -11,23 +11,25 @@
 //
 // Structure: one persistent CTA per SM over a contiguous row range; a ring of
 // NSLOT row slots in shared memory filled by TMA bulk copies (cp.async.bulk,
-// L2 evict_first, one mbarrier per slot) issued by a producer warp.  16
-// compute warps own fixed 16-byte column vectors (x^ and x^_1/2 for them, and
-// the column accumulators, live in registers for the whole kernel); two
-// epilogue warps run the y side.  Rows move in groups of TR through a
-// three-stage software pipeline whose hand-offs are all mbarriers (no
-// CTA-wide barrier after setup):
+// L2 evict_first, one mbarrier per slot) issued by a producer warp.  CW
+// compute warps (plan_fused: the fewest that keep <= 5 16-byte vectors per
+// thread, 8 at n = 5000) own fixed column vectors (x^, x^_1/2 and the column
+// accumulators live in registers for the whole kernel; fp32 rows use packed
+// FFMA2); three epilogue warps run the fp64 y side.  Rows move in groups of
+// TR through a three-stage software pipeline whose hand-offs are all
+// mbarriers (no CTA-wide barrier after setup):
 //
-//   compute warps   R(t)   dots of group t                    -> red_s[t&1]
-//                   C(t-2) A' [c_y, nu^] of group t-2 with w_s[t&1], then
-//                          release its slots to the producer
-//   epilogue warps  E(t)   (warp 16 + (t&1)) reduce red_s[t&1]; y side of
-//                          group t (YEpi::finish) -> w_s[t&1]
+//   compute warps   R(t)   dots of group t                    -> red_s[t % 3]
+//                   C(t-2) A' [c_y, nu^] of group t-2 with w_s[(t-2) % 3],
+//                          then release its slots to the producer
+//   epilogue warps  E(t)   (warp CW + t % 3) reduce red_s[t % 3]; y side of
+//                          group t (Epi::mid -> w_s, then Epi::tail)
 //   producer warp          refill released slots with the rows NSLOT ahead
 //
 // so the serial per-row epilogue (fp64 prox, divisions, global stores) runs
 // concurrently with the row and column passes of other groups.  Three groups
-// are resident; NSLOT - 3*TR rows are in flight from HBM.
+// are resident; NSLOT - 3*TR rows are in flight from HBM.  The first ring fill
+// is issued before the programmatic-dependency wait (A_hat is constant).
 #pragma once
 
 #include "gf_common.cuh"

@@ -9,19 +9,25 @@
 // The half iterates are double-buffered by iteration parity so a degenerate
 // iteration can hand back the previous one (solver.py:337-342).
 //
-// One iteration k is four launches (the per-iteration schedule of SURVEY
-// §7.2, which reads A_hat twice and never touches the unscaled A):
-//   R(k)  row pass    A_hat [x^, x^_1/2] with the whole y side in the epilogue:
-//                     y~ update (dual step + adaptive-rho rescale of k-1),
-//                     prox_f, nu^_1/2, c_y, and the r_pri / ||y|| / f(y)
-//                     partials (r_pri = ||D^-1 (A_hat x^_1/2 - y^_1/2)||).
-//   C(k)  column pass A_hat' [c_y, nu^_1/2] -> per-slab partials
-//   Z(k)  slab reduce (+ NCCL all-reduce of [2n + 6] under a row partition),
-//         rhs = c_x + A_hat' c_y, r_dual = ||E^-1 (A_hat' nu^ + mu^)||, and in
-//         the last CTA the controller: stop rule (solver.py:191-202, 373-376),
-//         degenerate checks, history row, adaptive rho (solver.py:221-239).
-//   S(k)  x+ = Ginv rhs (GEMV) with the whole x side in the epilogue:
-//         x~ update, prox_g for iteration k+1, mu^_1/2, c_x, ||mu||, g(x).
+// A tall iteration k is three launches (programmatic dependent launch between
+// them when no communicator is active):
+//   S(k-1) x+ = G^-1 rhs on a TMA row ring (gf_ring.cuh) with the whole x side
+//          in the epilogue: x~ update, prox_g of iteration k, mu^_1/2, c_x,
+//          ||mu||, g(x) partials.
+//   F(k)   the fused single pass over A_hat (gf_fused.cuh): row pass
+//          A_hat [x^, x^_1/2] with the whole y side in the epilogue -- y~
+//          update (dual step + adaptive-rho rescale of k-1), prox_f, nu^_1/2,
+//          c_y, r_pri / ||y|| / f(y) partials (r_pri = ||D^-1 (A_hat x^_1/2 -
+//          y^_1/2)||) -- and, while each row is still in shared memory, the
+//          column pass A_hat' [c_y, nu^_1/2] into per-CTA slabs.
+//   Z(k)   slab and record reductions (+ NCCL all-reduce of [2n + 8] under a
+//          row partition), rhs = c_x + A_hat' c_y, r_dual =
+//          ||E^-1 (A_hat' nu^ + mu^)||, and in the last CTA the controller:
+//          stop rule (solver.py:191-202, 373-376), degenerate checks, history
+//          row, adaptive rho (solver.py:221-239).
+// Rows too wide for the fused ring (and wide problems) use the two-pass
+// schedule: a row pass with the y side, then a column pass,
+// which reads A_hat twice; the unscaled A is never touched.
 // The controller lives on the device, so a chunk of iterations runs without a
 // host round trip; kernels of iterations after termination return at entry.
 
@@ -459,17 +465,16 @@ __device__ void decide_tall(Ctl* ctl, const Params& prm, const double* ys, const
   ctl->k = k + 1;
 }
 
-// Z2: per column the projection right-hand side (tall) or x+ (wide) and the
-// r_dual terms, then the controller in the last CTA.
-//   tall: red = [A_hat' c_y | A_hat' nu^ | y scalars]; rhs = c_x + A_hat' c_y
-//   wide: red = [A_hat' w   | A_hat' nu^ | y scalars]; x+ = c_x - A_hat' w
-//         (projection.py:124-126), y+ flags come from the Ginv pass (spart)
-template <typename T, bool WIDE>
+// Z step of a wide iteration (m < n): per column the x+ finiteness check and
+// the r_dual terms, then the controller in the last CTA (tall iterations use
+// zslab_tall_kernel).  red = [A_hat' w | A_hat' nu^ | y scalars];
+// x+ = c_x - A_hat' w (projection.py:124-126); the y+ flags come from the
+// G^-1 pass (spart).
 __global__ void __launch_bounds__(256)
-control_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ red, int64_t ld, int64_t n,
-               const double* __restrict__ cx, const double* __restrict__ e, const double* __restrict__ muh2,
-               T* __restrict__ rhs_T, double* __restrict__ zpart, const double* __restrict__ xpart,
-               int64_t nxpart, double* __restrict__ hist, const double* __restrict__ spart, int64_t nspart) {
+control_wide_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ red, int64_t ld, int64_t n,
+                    const double* __restrict__ cx, const double* __restrict__ e, const double* __restrict__ muh2,
+                    double* __restrict__ zpart, const double* __restrict__ xpart, int64_t nxpart,
+                    double* __restrict__ hist, const double* __restrict__ spart, int64_t nspart) {
   if (ctl->status != GF_STATUS_RUNNING) return;
   const int64_t k = ctl->k;
   const double* muh = muh2 + (k & 1) * n;
@@ -477,11 +482,7 @@ control_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ red
   unsigned zflag = 0;
   for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const double s1 = red[j], s2 = red[ld + j];
-    if (WIDE) {
-      if (!isfinite(S_(cx[j], s1))) zflag |= kBadXPlus;
-    } else {
-      rhs_T[j] = (T)A_(cx[j], s1);                    // c + A_hat' d (projection.py:121)
-    }
+    if (!isfinite(S_(cx[j], s1))) zflag |= kBadXPlus;
     const double ej = e[j];
     const double rdj = A_(D_(s2, ej), D_(muh[j], ej)); // A' nu + mu in original space
     rd2 += rdj * rdj;
@@ -531,8 +532,8 @@ control_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ red
     }
     __syncthreads();
   }
-  unsigned sflag = 0;   // wide: y+ = c_y + w flags of the Ginv pass
-  if (WIDE) {
+  unsigned sflag = 0;   // y+ = c_y + w flags of the Ginv pass
+  {
     unsigned f = 0;
     for (int64_t i = threadIdx.x; i < nspart; i += blockDim.x) f |= (unsigned)spart[i];
     sh[threadIdx.x] = (double)f;
@@ -548,7 +549,7 @@ control_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ red
   ctl->zflags = 0;
   const double* ys = red + 2 * ld;
   const unsigned xf = (unsigned)xs[kRedX];
-  if (WIDE) {
+  {
     // order of solver.py: prox checks (:337), residual stop (:373), then the
     // projection check (:414), then adapt_rho (:423)
     const bool prox_bad = (xf & kBadXHalf) || ys[5] > 0.0;
@@ -605,9 +606,7 @@ control_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ red
       return;
     }
     ctl->k = k + 1;
-    return;
   }
-  decide_tall(ctl, prm, ys, xs, r2, hist);
 }
 
 // Z(k) in one launch for tall problems without a communicator: the column
@@ -747,6 +746,19 @@ zslab_tall_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t k = ctl->k;
   const double* muh = muh2 + (k & 1) * n;
+  // the record reductions (x side; y side from slabs) do not wait for the
+  // column sums: CTA 0 does them first, off the last CTA's critical path,
+  // into red[2 ld + kScal ..] ([y scalars (kScal) | x sums + flags])
+  double* recs = red + 2 * ld + kScal;
+  if (blockIdx.x == 0) {
+    double yr[kRedY + 1], xs0[kRedX + 1];
+    if (FROM_SLABS) block_sum_records<kRedY>(rpart, nrpart, yr, shr);
+    block_sum_records<kRedX>(xpart, nxpart, xs0, shx);
+    if (threadIdx.x == 0) {
+      if (FROM_SLABS) y_layout(yr, recs);
+      for (int q = 0; q <= kRedX; ++q) recs[kScal + q] = xs0[q];
+    }
+  }
   double rd2 = 0.0;
   for (int64_t c0 = (int64_t)blockIdx.x * 32; c0 < n; c0 += (int64_t)gridDim.x * 32) {
     const int64_t j = c0 + lane;
@@ -775,9 +787,6 @@ zslab_tall_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ 
   __syncthreads();
   if (!last) return;
   __threadfence();
-  double yr[kRedY + 1], xs[kRedX + 1];
-  if (FROM_SLABS) block_sum_records<kRedY>(rpart, nrpart, yr, shr);
-  block_sum_records<kRedX>(xpart, nxpart, xs, shx);
   __shared__ double zs[8];
   {
     double z = 0.0;
@@ -791,7 +800,10 @@ zslab_tall_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ 
   for (int w = 0; w < 8; ++w) r2 += zs[w];
   ctl->ticket = 0;
   double* ys = red + 2 * ld;
-  if (FROM_SLABS) y_layout(yr, ys);
+  if (FROM_SLABS)
+    for (int q = 0; q < kScal; ++q) ys[q] = recs[q];
+  double xs[kRedX + 1];
+  for (int q = 0; q <= kRedX; ++q) xs[q] = recs[kScal + q];
   decide_tall(ctl, prm, ys, xs, r2, hist);
 }
 
@@ -1243,10 +1255,10 @@ static void launch_step_wide(gf_solver* s, int64_t k, cudaStream_t st) {
   GF_CHECK_LAUNCH();
   s->mark(4, st, false);
   s->mark(5, st, true);
-  control_kernel<T, true><<<(unsigned)s->grid_z, 256, 0, st>>>(
+  control_wide_kernel<<<(unsigned)s->grid_z, 256, 0, st>>>(
       ctl, s->prm, s->red.as<double>(), s->ld, s->n, s->cx.as<double>(), s->S->e.as<double>(), s->muh2.as<double>(),
-      s->rhs_T.as<T>(), s->zpart.as<double>(), s->xpart.as<double>(), s->grid_s, s->hist.as<double>(),
-      s->spart.as<double>(), s->grid_s);
+      s->zpart.as<double>(), s->xpart.as<double>(), s->grid_s, s->hist.as<double>(), s->spart.as<double>(),
+      s->grid_s);
   GF_CHECK_LAUNCH();
   s->mark(5, st, false);
   s->mark(0, st, true);
@@ -1376,7 +1388,7 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
   vec(s->rpart, std::max<int64_t>(s->grid_r, s->fplan.ok ? kFusedEpiMax * s->fplan.grid : 1) * (kRedY + 1));
   vec(s->xpart, s->grid_s * (kRedX + 1));
   vec(s->zpart, std::max(s->grid_z, s->grid_zt));
-  vec(s->red, 2 * s->ld + kScal);
+  vec(s->red, 2 * s->ld + 2 * kScal + kRedX + 1);   // + CTA 0's record sums (Z step)
   if (!s->tall) {
     vec(s->ypl, m1);
     vec(s->wv, m1);
