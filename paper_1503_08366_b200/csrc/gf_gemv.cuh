@@ -2,9 +2,10 @@
 //
 //  rowgemv : y_r = <A_r, x_k> for 1-2 right-hand sides, one warp per row,
 //            16-byte vector loads of A (L1 no-allocate: A is read once per
-//            pass) and of x (L1/L2 resident), 4 loads in flight per lane;
-//            the per-row result goes to an epilogue functor run by lane 0,
-//            whose reduction scalars are folded per CTA into `part`.
+//            pass) and of x (L1/L2 resident), 4-8 loads in flight per lane;
+//            the per-row results go to an epilogue functor, run for 32 rows
+//            at a time on the warp's lanes, whose reduction scalars are
+//            folded per CTA into `part`.
 //  colgemv : partial column sums  part[slab][k][j] = sum_{r in slab} f(A_rj) w_k[r]
 //            for 1-2 weight vectors; a CTA owns a 256-vector column strip of
 //            one row slab, so every warp load is a contiguous 512 B segment;
@@ -46,47 +47,62 @@ rowgemv_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* __res
 #pragma unroll
   for (int k = 0; k < (NR > 0 ? NR : 1); ++k) red[k] = 0.0;
   unsigned flags = 0;
-  for (int64_t r = (int64_t)blockIdx.x * kRowWarps + warp; r < rows; r += (int64_t)gridDim.x * kRowWarps) {
-    const V* ar = reinterpret_cast<const V*>(A + r * ld);
-    T s0 = 0, s1 = 0;
-    int64_t v = lane;
-    // one right-hand side: 8 row loads in flight per lane (a row of G^-1 is
-    // one warp's whole work, so the loop trip count is its latency chain)
-    constexpr int U = NRHS > 1 ? 4 : 8;
-    for (; v + (U - 1) * 32 < nvec; v += U * 32) {
-      V a[U], b0[U], b1[U];
+  // Rows r = w, w + W, ... (W warps in the grid) in batches of 32: the dot
+  // products of a batch first, lane t keeping row t's; then the 32 epilogues
+  // run in parallel on the lanes (a serial fp64 epilogue -- e.g. the
+  // logistic prox's Newton loop -- is paid once per batch, not per row).
+  const int64_t stride = (int64_t)gridDim.x * kRowWarps;
+  for (int64_t rb = (int64_t)blockIdx.x * kRowWarps + warp; rb < rows; rb += 32 * stride) {
+    double my0 = 0.0, my1 = 0.0;
+    int cnt = 0;
+    for (int t = 0; t < 32; ++t) {
+      const int64_t r = rb + t * stride;
+      if (r >= rows) break;
+      ++cnt;
+      const V* ar = reinterpret_cast<const V*>(A + r * ld);
+      T s0 = 0, s1 = 0;
+      int64_t v = lane;
+      // one right-hand side: 8 row loads in flight per lane
+      constexpr int U = NRHS > 1 ? 4 : 8;
+      for (; v + (U - 1) * 32 < nvec; v += U * 32) {
+        V a[U], b0[U], b1[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        a[u] = ld_stream(ar + v + 32 * u);
-        b0[u] = ldg_vec(xv0 + v + 32 * u);
-        if (NRHS > 1) b1[u] = ldg_vec(xv1 + v + 32 * u);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int i = 0; i < VN; ++i) {
-          s0 = fma(vget(a[u], i), vget(b0[u], i), s0);
-          if (NRHS > 1) s1 = fma(vget(a[u], i), vget(b1[u], i), s1);
+        for (int u = 0; u < U; ++u) {
+          a[u] = ld_stream(ar + v + 32 * u);
+          b0[u] = ldg_vec(xv0 + v + 32 * u);
+          if (NRHS > 1) b1[u] = ldg_vec(xv1 + v + 32 * u);
         }
-    }
-    for (; v < nvec; v += 32) {
-      const V a = ld_stream(ar + v);
-      const V b0 = ldg_vec(xv0 + v);
 #pragma unroll
-      for (int i = 0; i < VN; ++i) s0 = fma(vget(a, i), vget(b0, i), s0);
-      if (NRHS > 1) {
-        const V b1 = ldg_vec(xv1 + v);
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int i = 0; i < VN; ++i) s1 = fma(vget(a, i), vget(b1, i), s1);
+          for (int i = 0; i < VN; ++i) {
+            s0 = fma(vget(a[u], i), vget(b0[u], i), s0);
+            if (NRHS > 1) s1 = fma(vget(a[u], i), vget(b1[u], i), s1);
+          }
       }
+      for (; v < nvec; v += 32) {
+        const V a = ld_stream(ar + v);
+        const V b0 = ldg_vec(xv0 + v);
+#pragma unroll
+        for (int i = 0; i < VN; ++i) s0 = fma(vget(a, i), vget(b0, i), s0);
+        if (NRHS > 1) {
+          const V b1 = ldg_vec(xv1 + v);
+#pragma unroll
+          for (int i = 0; i < VN; ++i) s1 = fma(vget(a, i), vget(b1, i), s1);
+        }
+      }
+      s0 = warp_sum(s0);
+      if (NRHS > 1) s1 = warp_sum(s1);
+      if (lane == t) { my0 = (double)s0; my1 = (double)s1; }
     }
-    s0 = warp_sum(s0);
-    if (NRHS > 1) s1 = warp_sum(s1);
-    if (lane == 0) {
-      double dots[2] = {(double)s0, (double)s1};
-      epi.row(r, dots, red, flags);
+    if (lane < cnt) {
+      double dots[2] = {my0, my1};
+      epi.row(rb + lane * stride, dots, red, flags);
     }
   }
+#pragma unroll
+  for (int k = 0; k < NR; ++k) red[k] = warp_sum(red[k]);
+  flags = warp_or(flags);
   if (part == nullptr) return;
   __shared__ double sred[kRowWarps][NR + 1];
   if (lane == 0) {
