@@ -222,12 +222,20 @@ int gf_solver_snapshot(gf_solver* s, double* x_hat, double* y_hat, double* xt,
 int gf_solver_result(gf_solver* s, double* x, double* y, double* mu, double* nu,
                      gf_solver_state* st, void* stream);
 int gf_solver_destroy(gf_solver* s);
+/* One-shot solve (the proposed gf_solve of SURVEY §8b): create, run to
+ * termination, read SolveResult vectors (x, mu: n; y, nu: m; host or device)
+ * and, if history != NULL, the per-iteration rows (r_pri, r_dual, eps_pri,
+ * eps_dual, rho, objective) of iterations [0, st->k] into history
+ * ((settings->max_iter + 1) x 6 doubles, host), then destroy. */
+int gf_solve(gf_setup* S, const gf_terms* f, const gf_terms* g, const gf_settings* settings,
+             const double* x0, const double* nu0, double* x, double* y, double* mu, double* nu,
+             gf_solver_state* st, double* history, void* stream);
 /* device time (ms) spent in solver iterations so far (CUDA events) */
 int gf_solver_elapsed_ms(gf_solver* s, double* ms);
 /* instrumentation: kernels launched so far; with profiling enabled, summed
  * CUDA-event durations and counts per kernel class (8 slots: 0 Ginv GEMV +
  * x side, 1 row pass + y side, 2 column pass, 3 slab reduce, 4 y scalars,
- * 5 controller, 6 all-reduce, 7 reserved). */
+ * 5 Z step / controller, 6 all-reduce, 7 fused row + column pass). */
 int gf_solver_stats(gf_solver* s, int64_t* launches, double* kernel_ms, int64_t* kernel_count);
 int gf_solver_profile(gf_solver* s, int enable);
 

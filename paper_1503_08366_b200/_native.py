@@ -96,6 +96,8 @@ _SIGS = {
     "gf_solver_history": ([_P, C.c_int64, _P, _P], C.c_int),
     "gf_solver_snapshot": ([_P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
     "gf_solver_result": ([_P, _P, _P, _P, _P, C.POINTER(SolverState), _P], C.c_int),
+    "gf_solve": ([_P, C.POINTER(Terms), C.POINTER(Terms), C.POINTER(Settings), _P, _P, _P, _P, _P, _P,
+                  C.POINTER(SolverState), _P, _P], C.c_int),
     "gf_solver_destroy": ([_P], C.c_int),
     "gf_solver_elapsed_ms": ([_P, c_double_p], C.c_int),
     "gf_solver_stats": ([_P, c_int64_p, _P, _P], C.c_int),

@@ -680,6 +680,27 @@ int gf_solver_destroy(gf_solver* s) {
   return guarded([&] { solver_free(s); });
 }
 
+int gf_solve(gf_setup* S, const gf_terms* f, const gf_terms* g, const gf_settings* settings, const double* x0,
+             const double* nu0, double* x, double* y, double* mu, double* nu, gf_solver_state* st,
+             double* history, void* stream) {
+  return guarded([&] {
+    check_terms(f);
+    check_terms(g);
+    GF_REQUIRE(settings->max_iter >= 1, GF_E_PARAMETER, "max_iter must be at least 1");
+    const cudaStream_t cs = (cudaStream_t)stream;
+    struct Owner {
+      gf_solver* p = nullptr;
+      ~Owner() { if (p) solver_free(p); }
+    } s;
+    s.p = solver_create(S, f, g, settings, x0, nu0, cs);
+    gf_solver_state tmp{};
+    gf_solver_state* out = st ? st : &tmp;
+    solver_run(s.p, 0, out, cs);
+    solver_result(s.p, x, y, mu, nu, out, cs);
+    if (history != nullptr && out->k >= 0) solver_history(s.p, out->k + 1, history, cs);
+  });
+}
+
 int gf_solver_elapsed_ms(gf_solver* s, double* ms) {
   return guarded([&] { *ms = solver_elapsed(s); });
 }

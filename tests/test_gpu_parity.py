@@ -315,3 +315,30 @@ def test_duality_gap_and_gap_stop_helpers():
     p1 = gf.GraphFormProblem(np.ones((3, 3)), ab, z)
     assert gf.duality_gap(p1, np.zeros(3), np.zeros(3), np.zeros(3), np.zeros(3)) is None
     assert gf.gap_stop(p1, np.zeros(3), np.zeros(3), np.zeros(3), np.zeros(3), 1e-4, 1e-3) == (False, None)
+
+
+def test_one_shot_c_abi_solve_matches_public_api():
+    """gf_solve (create + run + result + history + destroy in one C call, the
+    boundary a ctypes/cgo binding would use) equals solve() bit for bit."""
+    import ctypes as C
+    from paper_1503_08366_b200 import _native, solver as slv
+    fx = _cases.load("solve_lasso_tall_1000x200")
+    prob = _cases.build_problem(fx)
+    st = gf.SolverSettings()
+    ref = gf.solve(prob, st)
+    setup = gf.prepare(prob)
+    L = _native.lib()
+    fT, keep_f = _native.host_terms(prob.f)
+    gT, keep_g = _native.host_terms(prob.g)
+    s = slv._gf_settings(st)
+    m, n = prob.m, prob.n
+    x, mu, y, nu = np.empty(n), np.empty(n), np.empty(m), np.empty(m)
+    hist = np.zeros((st.max_iter + 1, 6))
+    state = _native.SolverState()
+    _native.check(L.gf_solve(setup.handle, C.byref(fT), C.byref(gT), C.byref(s), None, None, _native.ptr(x),
+                             _native.ptr(y), _native.ptr(mu), _native.ptr(nu), C.byref(state), _native.ptr(hist),
+                             _native.stream()))
+    assert state.iterations == ref.iterations == int(fx["iterations"])
+    for a, b in ((x, ref.x), (y, ref.y), (mu, ref.mu), (nu, ref.nu)):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_allclose(hist[:ref.iterations], fx["history"], rtol=1e-8, atol=1e-12)
