@@ -55,7 +55,8 @@ def build(jobs=8, verbose=False):
     objs = [o for o, _ in results]
     newest = max(os.path.getmtime(o) for o in objs)
     if not os.path.exists(OUT) or os.path.getmtime(OUT) < newest:
-        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lnccl", "-lcudart"]
+        # NCCL is dlopen()ed at run time (gf_api.cu), not linked
+        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

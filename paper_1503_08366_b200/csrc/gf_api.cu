@@ -1,6 +1,8 @@
 // C-ABI entry points (include/graphform_b200.h): argument checks, object
 // lifetimes, error-code mapping, projector/setup orchestration and NCCL glue.
 
+#include <dlfcn.h>
+
 #include <chrono>
 #include <mutex>
 #include <cstring>
@@ -40,10 +42,46 @@ int num_sms() {
   return sms;
 }
 
+// NCCL is resolved at run time (dlopen), not linked: a process that loads this
+// library before torch must not pin the system libnccl.so.2 (2.27) under the
+// soname torch's own 2.28 copy needs.  An already-loaded libnccl.so.2 (torch's,
+// whenever torch.distributed set up the ranks) is used first.
+struct NcclApi {
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  const char* (*GetErrorString)(ncclResult_t);
+};
+
+static const NcclApi& nccl() {
+  static std::mutex mu;
+  static NcclApi api{};
+  static bool ready = false;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ready) {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (h == nullptr) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h == nullptr) throw_error(GF_E_NCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
+    auto sym = [&](const char* name) {
+      void* f = dlsym(h, name);
+      if (f == nullptr) throw_error(GF_E_NCCL, std::string("libnccl.so.2 lacks ") + name);
+      return f;
+    };
+    api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+    api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+    api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+    ready = true;
+  }
+  return api;
+}
+
 void allreduce_sum(gf_comm* c, double* buf, size_t count, cudaStream_t st) {
   if (!comm_active(c) || count == 0) return;
-  const ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, st);
-  if (r != ncclSuccess) throw_error(GF_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+  const ncclResult_t r = nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, st);
+  if (r != ncclSuccess) throw_error(GF_E_NCCL, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
 }
 
 // Grow-only per-device scratch (plain cudaMalloc, kept for the process) for
@@ -716,8 +754,8 @@ int gf_solver_profile(gf_solver* s, int enable) {
 int gf_comm_unique_id(char* id128) {
   return guarded([&] {
     ncclUniqueId id;
-    const ncclResult_t r = ncclGetUniqueId(&id);
-    if (r != ncclSuccess) throw_error(GF_E_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    const ncclResult_t r = nccl().GetUniqueId(&id);
+    if (r != ncclSuccess) throw_error(GF_E_NCCL, std::string("ncclGetUniqueId: ") + nccl().GetErrorString(r));
     std::memcpy(id128, id.internal, sizeof(id.internal));
   });
 }
@@ -731,8 +769,8 @@ int gf_comm_create(const char* id128, int nranks, int rank, gf_comm** out) {
     {   // a communicator even for one rank, so every collective call site is exercisable on one GPU
       ncclUniqueId id;
       std::memcpy(id.internal, id128, sizeof(id.internal));
-      const ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
-      if (r != ncclSuccess) throw_error(GF_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      const ncclResult_t r = nccl().CommInitRank(&c->comm, nranks, id, rank);
+      if (r != ncclSuccess) throw_error(GF_E_NCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
     }
     *out = c.release();
   });
@@ -741,7 +779,7 @@ int gf_comm_create(const char* id128, int nranks, int rank, gf_comm** out) {
 int gf_comm_destroy(gf_comm* c) {
   return guarded([&] {
     if (!c) return;
-    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->comm) nccl().CommDestroy(c->comm);
     delete c;
   });
 }
