@@ -292,6 +292,41 @@ constexpr int NB = 64;
 constexpr int CB = 128, CMB = 16, CSL = CB + 1;
 constexpr size_t kCholSmem = (size_t)CB * CSL * sizeof(double);
 
+// 16 x 16 leaf of the diagonal-block factorisation, lane i holding row i in
+// registers; pivot J then the rank-1 update of the later columns.  Template
+// recursion keeps every register index static (a loop here was left rolled
+// by the compiler and put the row in local memory).  One reciprocal square
+// root per pivot: the pivots are a serial chain, this is its latency.
+template <int J, int K>
+__device__ __forceinline__ void leaf_update(double (&r)[CMB], int lane) {
+  if constexpr (K < CMB) {
+    const double lkj = __shfl_sync(0xffffffffu, r[J], K);
+    if (lane >= K) r[K] = fma(-r[J], lkj, r[K]);
+    leaf_update<J, K + 1>(r, lane);
+  }
+}
+
+template <int J>
+__device__ __forceinline__ void leaf_pivot(double (&r)[CMB], int lane, double* rinv, int* info, int64_t base) {
+  if constexpr (J < CMB) {
+    double dj = __shfl_sync(0xffffffffu, r[J], J);
+    double ri;
+    if (!(dj > 0.0) || !isfinite(dj)) {
+      if (lane == 0 && *info == 0) *info = (int)(base + J + 1);
+      dj = 1.0;
+      ri = 1.0;
+    } else {
+      ri = rsqrt(dj);
+      dj = dj * ri;
+    }
+    if (lane == J) r[J] = dj;
+    if (lane > J) r[J] *= ri;
+    if (lane == 0) rinv[J] = ri;
+    leaf_update<J, J + 1>(r, lane);
+    leaf_pivot<J + 1>(r, lane, rinv, info, base);
+  }
+}
+
 __global__ void __launch_bounds__(512) potrf_block(double* G, int64_t ld, int64_t k0, int nb, int* info) {
   extern __shared__ double S[];
   __shared__ double rinv[CB];   // reciprocals of the finished pivots (no divisions in the chains)
@@ -308,25 +343,7 @@ __global__ void __launch_bounds__(512) potrf_block(double* G, int64_t ld, int64_
         double r[CMB];
 #pragma unroll
         for (int k = 0; k < CMB; ++k) r[k] = (lane < CMB && k <= lane) ? S[(p + lane) * CSL + p + k] : 0.0;
-#pragma unroll
-        for (int j = 0; j < CMB; ++j) {
-          double dj = __shfl_sync(0xffffffffu, r[j], j);
-          if (!(dj > 0.0) || !isfinite(dj)) {
-            if (lane == 0 && *info == 0) *info = (int)(k0 + p + j + 1);
-            dj = 1.0;
-          } else {
-            dj = sqrt(dj);
-          }
-          const double ri = 1.0 / dj;
-          if (lane == j) r[j] = dj;
-          if (lane > j) r[j] *= ri;
-          if (lane == 0) rinv[p + j] = ri;
-#pragma unroll
-          for (int k = j + 1; k < CMB; ++k) {
-            const double lkj = __shfl_sync(0xffffffffu, r[j], k);
-            if (lane >= k) r[k] = fma(-r[j], lkj, r[k]);
-          }
-        }
+        leaf_pivot<0>(r, lane, rinv + p, info, k0 + p);
         if (lane < CMB)
 #pragma unroll
           for (int k = 0; k < CMB; ++k)
