@@ -675,9 +675,9 @@ __device__ __forceinline__ void slab_columns(const double* __restrict__ cpart, i
         a1[u] += cpart[(2 * (sl + 8 * u)) * ld + j];
         a2[u] += cpart[(2 * (sl + 8 * u) + 1) * ld + j];
       }
-    for (int u = 0; sl < slabs; sl += 8, ++u) {
-      a1[u & 3] += cpart[(2 * sl) * ld + j];
-      a2[u & 3] += cpart[(2 * sl + 1) * ld + j];
+    for (; sl < slabs; sl += 8) {   // remainder into chain 0 (static indices: no local memory)
+      a1[0] += cpart[(2 * sl) * ld + j];
+      a2[0] += cpart[(2 * sl + 1) * ld + j];
     }
     s1 = (a1[0] + a1[1]) + (a1[2] + a1[3]);
     s2 = (a2[0] + a2[1]) + (a2[2] + a2[3]);

@@ -277,15 +277,20 @@ syrk_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         // the upper triangle is mirrored down afterwards (gram_finish).
         // all 32 loads are issued before any store (a plain `+=` loop would
         // serialize on possible aliasing between the stores and later loads)
+        // (two halves of 16: 32 fp64 values plus the 32 accumulator words
+        // overflowed the 128-register budget into local memory)
         if (i < q) {
-          double g[32];
           const int64_t jn = min((int64_t)32, q - (j0 + cc * 32));
           double* col = G + (j0 + cc * 32) * ldg + i;
 #pragma unroll
-          for (int t = 0; t < 32; ++t) g[t] = t < jn ? col[t * ldg] : 0.0;
+          for (int h = 0; h < 2; ++h) {
+            double g[16];
 #pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (t < jn) col[t * ldg] = g[t] + (double)__uint_as_float(v[t]);
+            for (int t = 0; t < 16; ++t) g[t] = 16 * h + t < jn ? col[(16 * h + t) * ldg] : 0.0;
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+              if (16 * h + t < jn) col[(16 * h + t) * ldg] = g[t] + (double)__uint_as_float(v[16 * h + t]);
+          }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
