@@ -207,3 +207,26 @@ def test_c3_lp_50000x20000_prefix():
     res, hist = solve_with_history(prob, st)
     check_fp64(fx, res, hist, full=False)
     check_properties(prob, res, st, 1e-8)
+
+
+def test_huber_fit_100000x2000_fp64():
+    """the Huber prox kind at scale (robust regression,
+    huber_fit family), full fp64 solve against the reference."""
+    fx = fixture("huber_fit_100000x2000")
+    prob = device_instance(fx)
+    st = gf.SolverSettings()
+    res, hist = solve_with_history(prob, st)
+    check_fp64(fx, res, hist)
+    check_properties(prob, res, st, 1e-8)
+
+
+def test_entropy_max_2000x50000_fp64_wide():
+    """negative entropy (a Newton prox) in the wide
+    orientation (m < n: the I + A A' projector and the wide schedule) at
+    scale, full fp64 solve against the reference."""
+    fx = fixture("entropy_max_2000x50000")
+    prob = device_instance(fx)
+    st = gf.SolverSettings()
+    res, hist = solve_with_history(prob, st)
+    check_fp64(fx, res, hist)
+    check_properties(prob, res, st, 1e-8)
