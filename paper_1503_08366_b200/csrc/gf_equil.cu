@@ -32,7 +32,23 @@ sq_row_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, int64_t n, cons
   for (int64_t r = (int64_t)blockIdx.x * kRowWarps + warp; r < rows; r += (int64_t)gridDim.x * kRowWarps) {
     const V* ar = reinterpret_cast<const V*>(A + r * ld);
     double acc = 0.0;
-    for (int64_t v = lane; v < nvec; v += 32) {
+    int64_t v = lane;
+    for (; v + 96 < nvec; v += 128) {   // four 16-byte loads in flight per lane
+      V a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = ld_stream(ar + v + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < VN; ++i) {
+          const int64_t j = (v + 32 * u) * VN + i;
+          if (j < n) {
+            const double x = (double)vget(a[u], i);
+            acc = fma(x * x, __ldg(w + j), acc);
+          }
+        }
+    }
+    for (; v < nvec; v += 32) {
       const V a = ld_stream(ar + v);
 #pragma unroll
       for (int i = 0; i < VN; ++i) {

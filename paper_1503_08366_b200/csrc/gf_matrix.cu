@@ -89,20 +89,41 @@ void matrix_to_f64(const gf_matrix* M, double* dst, cudaStream_t st) {
 // A_ij <- (d_i * A_ij) * e_j in fp64, rounded to the working dtype
 // (solver.py:145 evaluation order).
 template <typename T>
-__global__ void scale_kernel(T* __restrict__ A, int64_t rows, int64_t ld, int64_t n, const double* __restrict__ d,
-                             const double* __restrict__ e) {
-  const int64_t r = blockIdx.y + (int64_t)blockIdx.z * 65535;
-  if (r >= rows) return;
-  const double dr = d[r];
-  T* row = A + r * ld;
-  for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
-    row[j] = (T)((dr * (double)row[j]) * e[j]);
+__device__ __forceinline__ T scale1(T a, double dr, double ej) {
+  return (T)((dr * (double)a) * ej);
+}
+
+// One CTA per row (grid-stride), 16-byte vectors: A is read and written
+// once (2 m n s bytes); columns past n are the zero padding and stay zero.
+template <typename T>
+__global__ void __launch_bounds__(256) scale_kernel(T* __restrict__ A, int64_t rows, int64_t ld, int64_t n,
+                                                    const double* __restrict__ d, const double* __restrict__ e) {
+  using V = typename Vec16<T>::type;
+  constexpr int VN = Vec16<T>::n;
+  const int64_t nv = (n + VN - 1) / VN;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const double dr = d[r];
+    V* row = reinterpret_cast<V*>(A + r * ld);
+    for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+      V a = row[v];
+      const int64_t j = v * VN;
+      if constexpr (VN == 4) {
+        a.x = scale1(a.x, dr, e[j]);
+        if (j + 1 < n) a.y = scale1(a.y, dr, e[j + 1]);
+        if (j + 2 < n) a.z = scale1(a.z, dr, e[j + 2]);
+        if (j + 3 < n) a.w = scale1(a.w, dr, e[j + 3]);
+      } else {
+        a.x = scale1(a.x, dr, e[j]);
+        if (j + 1 < n) a.y = scale1(a.y, dr, e[j + 1]);
+      }
+      row[v] = a;
+    }
+  }
 }
 
 void scale_matrix(gf_matrix* M, const double* d, const double* e, cudaStream_t st) {
   if (M->m == 0) return;
-  const int64_t ry = std::min<int64_t>(M->m, 65535);
-  dim3 grid((unsigned)std::min<int64_t>(ceil_div(M->n, 256), 8), (unsigned)ry, (unsigned)ceil_div(M->m, 65535));
+  const unsigned grid = (unsigned)std::min<int64_t>(M->m, (int64_t)num_sms() * 8);
   if (M->dtype == GF_F32) scale_kernel<float><<<grid, 256, 0, st>>>((float*)M->data, M->m, M->ld, M->n, d, e);
   else scale_kernel<double><<<grid, 256, 0, st>>>((double*)M->data, M->m, M->ld, M->n, d, e);
   GF_CHECK_LAUNCH();
