@@ -15,8 +15,9 @@ Cases:
   c4_svm_200000x5000        configs[3], fp64, full solve
   c2_logistic_100000x10000_prefix  configs[1], default settings, 30 iterations
   c3_lp_50000x20000_prefix  configs[2], default settings, 10 iterations
-  huber_fit_100000x2000     Huber loss + l1, full solve
-  entropy_max_2000x50000    negative entropy, wide (m < n) orientation, full solve
+  huber_fit_100000x2000_prefix   Huber loss + l1, 60 iterations
+                                 (the full solve takes over 30 min on 8 cores)
+  entropy_max_2000x50000_prefix  negative entropy, wide (m < n) orientation, 60 iterations
 """
 
 from __future__ import annotations
@@ -42,8 +43,8 @@ CASES = [
     ("c2_logistic_100000x10000_prefix", ("logistic", 100000, 10000, 0), {"max_iter": 30}),
     ("c3_lp_50000x20000_prefix", ("lp", 50000, 20000, 0), {"max_iter": 10}),
     # the other prox kinds and families at scale
-    ("huber_fit_100000x2000", ("huber_fit", 100000, 2000, 0), {}),
-    ("entropy_max_2000x50000", ("entropy_max", 2000, 50000, 0), {}),
+    ("huber_fit_100000x2000_prefix", ("huber_fit", 100000, 2000, 0), {"max_iter": 60}),
+    ("entropy_max_2000x50000_prefix", ("entropy_max", 2000, 50000, 0), {"max_iter": 60}),
 ]
 
 

@@ -40,6 +40,11 @@ def fixture(name):
     return _cases.load(f"full_{name}")
 
 
+def close(a, b, tol, floor=1e-10):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return float(np.linalg.norm(a - b)) <= tol * float(np.linalg.norm(b)) + floor * max(1.0, np.sqrt(b.size))
+
+
 def rel(a, b):
     a, b = np.asarray(a, float), np.asarray(b, float)
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
@@ -105,8 +110,9 @@ def check_fp64(fx, res, hist, full=True, htol=1e-6, vtol=1e-5):
     assert hist.shape == h.shape
     np.testing.assert_allclose(hist[0], h[0], rtol=1e-6, atol=1e-12)
     np.testing.assert_allclose(hist, h, rtol=htol, atol=1e-12)
-    assert rel(res.x, fx["x"]) <= vtol and rel(res.mu, fx["mu"]) <= vtol
-    assert rel(res.y[:4096], fx["y_head"]) <= vtol and rel(res.nu[:4096], fx["nu_head"]) <= vtol
+    # (absolute floor: some duals are identically ~0, e.g. mu of a Huber fit at 1e-16)
+    assert close(res.x, fx["x"], vtol) and close(res.mu, fx["mu"], vtol)
+    assert close(res.y[:4096], fx["y_head"], vtol) and close(res.nu[:4096], fx["nu_head"], vtol)
     assert np.linalg.norm(res.y) == pytest.approx(float(fx["y_norm"]), rel=vtol)
     assert np.linalg.norm(res.nu) == pytest.approx(float(fx["nu_norm"]), rel=vtol)
     obj = float(fx["objective"])
@@ -209,24 +215,24 @@ def test_c3_lp_50000x20000_prefix():
     check_properties(prob, res, st, 1e-8)
 
 
-def test_huber_fit_100000x2000_fp64():
+def test_huber_fit_100000x2000_fp64_prefix():
     """the Huber prox kind at scale (robust regression,
-    huber_fit family), full fp64 solve against the reference."""
-    fx = fixture("huber_fit_100000x2000")
+    huber_fit family), 60 fp64 iterations against the reference."""
+    fx = fixture("huber_fit_100000x2000_prefix")
     prob = device_instance(fx)
-    st = gf.SolverSettings()
+    st = gf.SolverSettings(max_iter=60)
     res, hist = solve_with_history(prob, st)
-    check_fp64(fx, res, hist)
+    check_fp64(fx, res, hist, full=False)
     check_properties(prob, res, st, 1e-8)
 
 
-def test_entropy_max_2000x50000_fp64_wide():
+def test_entropy_max_2000x50000_fp64_wide_prefix():
     """negative entropy (a Newton prox) in the wide
     orientation (m < n: the I + A A' projector and the wide schedule) at
-    scale, full fp64 solve against the reference."""
-    fx = fixture("entropy_max_2000x50000")
+    scale, 60 fp64 iterations against the reference."""
+    fx = fixture("entropy_max_2000x50000_prefix")
     prob = device_instance(fx)
-    st = gf.SolverSettings()
+    st = gf.SolverSettings(max_iter=60)
     res, hist = solve_with_history(prob, st)
-    check_fp64(fx, res, hist)
+    check_fp64(fx, res, hist, full=False)
     check_properties(prob, res, st, 1e-8)
