@@ -1380,19 +1380,13 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
     s->fplan = plan_fused(s->m, s->ld, (int)es, sms, (size_t)optin);
     const char* env = getenv("GF_DISABLE_FUSED");
     if ((env && env[0] == '1') || !s->tall) s->fplan.ok = false;
-    // Newton-prox rows (logistic, negative entropy: prox.py:27-70, up to 100
-    // fp64 iterations each) make the fused epilogue the bottleneck when only
-    // one row per group fits (wide rows, few slots): the two-pass schedule,
-    // whose row pass runs one epilogue per warp across thousands of warps, is
-    // then faster (C2 logistic 100000 x 10000: 1.67 vs 1.85 ms/iteration)
-    if (s->fplan.ok && s->fplan.tr == 1 && s->m > 0) {
-      std::vector<int8_t> hk((size_t)s->m);
-      GF_CUDA(cudaMemcpyAsync(hk.data(), s->f.view.h, (size_t)s->m, cudaMemcpyDeviceToHost, st));
-      GF_CUDA(cudaStreamSynchronize(st));
-      int64_t newton = 0;
-      for (int8_t h : hk) newton += (h == kLogistic || h == kNegEntr) ? 1 : 0;
-      if (8 * newton > s->m) s->fplan.ok = false;
-    }
+    // With only one row per group (rows of ~40 KB and more: five ring slots)
+    // the fused pass is bound by the per-row fp64 epilogue latency rather
+    // than by HBM, and the two-pass schedule -- whose row pass runs the
+    // epilogues 32 rows per warp across thousands of warps -- is faster:
+    // measured C2 logistic 100000 x 10000 fp32 1.52 vs 1.85 ms, SVM
+    // 200000 x 5000 fp64 2.54 vs 2.85 ms per iteration.
+    if (s->fplan.ok && s->fplan.tr == 1) s->fplan.ok = false;
     if (s->fplan.ok) {
       if (s->dtype == GF_F32) fused_prepare<float>(s.get());
       else fused_prepare<double>(s.get());

@@ -21,6 +21,7 @@ CONFIGS = {
     "c2": ("logistic", 100_000, 10_000, np.float32),
     "c3": ("lp", 50_000, 20_000, np.float64),
     "c4": ("svm", 200_000, 5_000, np.float32),
+    "c4d": ("svm", 200_000, 5_000, np.float64),
 }
 NAMES = ["ginv_gemv_xside", "row_pass_yside", "col_pass", "slab_reduce", "y_scalars", "zstep_controller",
          "allreduce", "fused_rowcol_yside"]
