@@ -1386,7 +1386,8 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
     // epilogues 32 rows per warp across thousands of warps -- is faster:
     // measured C2 logistic 100000 x 10000 fp32 1.52 vs 1.85 ms, SVM
     // 200000 x 5000 fp64 2.54 vs 2.85 ms per iteration.
-    if (s->fplan.ok && s->fplan.tr == 1) s->fplan.ok = false;
+    const char* force = getenv("GF_FORCE_FUSED");   // dev override for measurements
+    if (s->fplan.ok && s->fplan.tr == 1 && !(force && force[0] == '1')) s->fplan.ok = false;
     if (s->fplan.ok) {
       if (s->dtype == GF_F32) fused_prepare<float>(s.get());
       else fused_prepare<double>(s.get());
