@@ -66,10 +66,15 @@ def ncu_traffic(kernel, m, n):
 
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(p):
+    fallback = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+    try:
         with open(p) as f:
-            return json.load(f), "measured"
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+            d = json.load(f)
+        if float(d.get("hbm_gbs", 0)) > 0:
+            return d, "measured"
+    except (OSError, ValueError, TypeError, AttributeError):
+        pass
+    return fallback, "fallback"
 
 
 class ClockSampler:
