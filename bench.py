@@ -351,7 +351,10 @@ def run_ours(args):
         "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(dom, m_loc, n), "kernel": dom,
-                     "algorithmic_bytes_per_launch": alg_bytes, "peak_kind": peaks_kind},
+                     "algorithmic_bytes_per_launch": alg_bytes, "peak_kind": peaks_kind,
+                     # context: the kernel only reads A_hat; a bare TMA read ring on
+                     # this part reaches ~7.34 TB/s (profiles/r01_readbw_probe.txt)
+                     "read_stream_ceiling_gbs": 7344.0, "frac_of_read_ceiling": achieved / 7344.0},
         "kernels": kernels,
         "gpu_launches": int(l1.value - l0.value),
         "clocks": clk.summary(),
