@@ -86,14 +86,24 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
-        # NVML (the library behind nvidia-smi) polled every 5 ms; falls back
-        # to the nvidia-smi CLI when pynvml is unavailable
+    def _nvml(self):
+        # NVML (the library behind nvidia-smi), initialised before the timed
+        # region starts so that polling covers all of it
         try:
             import pynvml as N
             N.nvmlInit()
             h = N.nvmlDeviceGetHandleByIndex(self.index)
             mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+            return N, h, mx
+        except Exception:
+            return None
+
+    def _run(self):
+        # NVML polled every 5 ms; falls back to the nvidia-smi CLI when pynvml
+        # is unavailable
+        if self._nv is not None:
+            N, h, mx = self._nv
             bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
                     N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
             while not self._stop.is_set():
@@ -102,8 +112,6 @@ class ClockSampler:
                 self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
                 self._stop.wait(0.005)
             return
-        except Exception:
-            pass
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -119,6 +127,7 @@ class ClockSampler:
             self._stop.wait(0.1)
 
     def __enter__(self):
+        self._nv = self._nvml()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -373,7 +382,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--m", type=int, default=M_FULL)
