@@ -23,7 +23,7 @@ OUT = os.path.join(PKG, "libgraphform_b200.so")
 BUILD = os.path.join(ROOT, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", HERE]
 
 
@@ -56,7 +56,7 @@ def build(jobs=8, verbose=False):
     newest = max(os.path.getmtime(o) for o in objs)
     if not os.path.exists(OUT) or os.path.getmtime(OUT) < newest:
         # NCCL is dlopen()ed at run time (gf_api.cu), not linked
-        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart", "-ldl"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart", "-ldl", "-lgomp"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

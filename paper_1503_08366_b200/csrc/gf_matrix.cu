@@ -7,6 +7,8 @@
 // unscaled A again because the residuals are taken through A_hat with the
 // diagonal scalings folded in (A x = D^-1 A_hat E^-1 x).
 
+#include <mutex>
+#include <cstring>
 #include "gf_internal.h"
 #include "gf_gemv.cuh"
 
@@ -56,11 +58,89 @@ static void convert_any(int sdt, const void* src, int64_t lds, int ddt, void* ds
   else launch_convert<float, float>(src, lds, dst, ldd, rows, cols, st);
 }
 
+static bool is_pinned_host_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// Pinned staging buffers for pageable host sources, kept for the process.
+struct Staging {
+  std::mutex mu;
+  static constexpr int kBufs = 3;
+  static constexpr size_t kBytes = (size_t)96 << 20;
+  char* buf[kBufs] = {nullptr, nullptr, nullptr};
+  cudaEvent_t done[kBufs] = {nullptr, nullptr, nullptr};
+};
+static Staging& staging() {
+  static Staging s;
+  return s;
+}
+
+// A pageable host matrix (a plain numpy array -- what a reference user
+// passes) moves through cudaMemcpy at ~10 GB/s: the driver bounces it
+// through a small pinned buffer.  Here host threads (OpenMP) copy row chunks
+// into three pinned 96 MB buffers that the copy engine drains asynchronously,
+// so the host copy of chunk i overlaps the DMA of chunks i-1, i-2.
+static void upload_pageable(gf_matrix* M, const void* src, int src_dtype, int64_t src_ld, cudaStream_t st) {
+  const size_t ses = src_dtype == GF_F32 ? 4 : 8;
+  const size_t row_src = (size_t)M->n * ses;
+  Staging& S = staging();
+  std::lock_guard<std::mutex> lk(S.mu);
+  for (int b = 0; b < Staging::kBufs; ++b)
+    if (S.buf[b] == nullptr) {
+      GF_CUDA(cudaMallocHost(&S.buf[b], Staging::kBytes));
+      GF_CUDA(cudaEventCreateWithFlags(&S.done[b], cudaEventDisableTiming));
+    }
+  const int64_t rows_per = std::max<int64_t>(1, (int64_t)(Staging::kBytes / std::max<size_t>(row_src, 1)));
+  DBuf dstage;
+  if (src_dtype != M->dtype) dstage.alloc((size_t)std::min(rows_per, M->m) * row_src);
+  bool used[Staging::kBufs] = {false, false, false};
+  int b = 0;
+  for (int64_t r0 = 0; r0 < M->m; r0 += rows_per, b = (b + 1) % Staging::kBufs) {
+    const int64_t nr = std::min(rows_per, M->m - r0);
+    if (used[b]) GF_CUDA(cudaEventSynchronize(S.done[b]));   // its previous DMA has drained
+    char* dst = S.buf[b];
+    const char* sp = (const char*)src + (size_t)r0 * src_ld * ses;
+    const size_t total = (size_t)nr * row_src;
+    if ((size_t)src_ld * ses == row_src) {   // contiguous rows: one flat parallel copy
+      const int64_t parts = 64;
+#pragma omp parallel for schedule(static)
+      for (int64_t q = 0; q < parts; ++q) {
+        const size_t a = total * q / parts, e = total * (q + 1) / parts;
+        memcpy(dst + a, sp + a, e - a);
+      }
+    } else {
+#pragma omp parallel for schedule(static)
+      for (int64_t r = 0; r < nr; ++r) memcpy(dst + r * row_src, sp + (size_t)r * src_ld * ses, row_src);
+    }
+    if (src_dtype == M->dtype) {
+      GF_CUDA(cudaMemcpy2DAsync((char*)M->data + (size_t)r0 * M->ld * M->esize(), M->ld * M->esize(), dst, row_src,
+                                row_src, nr, cudaMemcpyHostToDevice, st));
+    } else {
+      GF_CUDA(cudaMemcpyAsync(dstage.p, dst, total, cudaMemcpyHostToDevice, st));
+      convert_any(src_dtype, dstage.p, M->n, M->dtype, (char*)M->data + (size_t)r0 * M->ld * M->esize(), M->ld,
+                  nr, M->n, st);
+    }
+    GF_CUDA(cudaEventRecord(S.done[b], st));
+    used[b] = true;
+  }
+  GF_CUDA(cudaStreamSynchronize(st));
+}
+
 void matrix_upload(gf_matrix* M, const void* src, int src_dtype, int64_t src_ld, cudaStream_t st) {
   const size_t ses = src_dtype == GF_F32 ? 4 : 8;
   if (M->m == 0) return;
   if (is_device_ptr(src)) {
     convert_any(src_dtype, src, src_ld, M->dtype, M->data, M->ld, M->m, M->n, st);
+    return;
+  }
+  if (!is_pinned_host_ptr(src) && (size_t)M->m * M->n * ses >= ((size_t)64 << 20)) {
+    if (M->ld > M->n) GF_CUDA(cudaMemsetAsync(M->data, 0, (size_t)M->m * M->ld * M->esize(), st));
+    upload_pageable(M, src, src_dtype, src_ld, st);
     return;
   }
   if (src_dtype == M->dtype) {
