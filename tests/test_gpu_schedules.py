@@ -1,0 +1,56 @@
+"""The alternative iteration schedules agree with the default one: the
+two-pass schedule (GF_DISABLE_FUSED=1, what wide rows and Newton-heavy
+problems use), the plain row GEMV for G^-1 (GF_DISABLE_RING=1), and launches
+without programmatic dependent launch (GF_DISABLE_PDL=1, bit-identical).
+Each variant runs in a subprocess (the switches are read once per process)."""
+
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import json, sys
+sys.path.insert(0, ROOT)
+import numpy as np
+import paper_1503_08366_b200 as gf
+from tests import _cases
+out = {}
+for name in ("lasso_tall_20000x500", "svm_2000x100", "lp_600x240"):
+    fx = _cases.load("solve_" + name)
+    r = gf.solve(_cases.build_problem(fx), gf.SolverSettings(**_cases.settings_of(fx)))
+    out[name] = {"it": r.iterations, "status": r.status.value, "x": r.x.tolist(), "y": r.y.tolist(),
+                 "obj": r.objective}
+print(json.dumps(out))
+"""
+
+
+def run_variant(env_extra):
+    env = dict(os.environ, **env_extra)
+    code = SCRIPT.replace("ROOT", repr(ROOT))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def test_schedule_variants_agree():
+    base = run_variant({})
+    nopdl = run_variant({"GF_DISABLE_PDL": "1"})
+    assert nopdl == base   # PDL changes launch timing only: bit-identical
+    for env in ({"GF_DISABLE_FUSED": "1"}, {"GF_DISABLE_RING": "1"}):
+        alt = run_variant(env)
+        for name, b in base.items():
+            a = alt[name]
+            assert a["it"] == b["it"] and a["status"] == b["status"], (env, name)
+            for k in ("x", "y"):
+                np.testing.assert_allclose(a[k], b[k], rtol=1e-9, atol=1e-11, err_msg=f"{env} {name} {k}")
+            assert a["obj"] == pytest.approx(b["obj"], rel=1e-10)
