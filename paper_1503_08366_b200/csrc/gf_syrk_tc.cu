@@ -1,30 +1,43 @@
-// Tensor-core Gram matrix G = A'A for fp32 A (tall projector setup),
-// tcgen05 kind::tf32 with a 3xTF32 split for fp32-grade accuracy.
+// Tensor-core Gram matrix G = A'A for fp32 A (tall projector setup) on
+// tcgen05 with a three-product split for fp32-grade accuracy.
 //
 // Reference: projection.py:86-90 (gram = A.T @ A; gram += I) on OpenBLAS dgemm.
 // The north star asks for a tensor-core SYRK; plain TF32 perturbs G enough to
 // move fp32 iterates (x error 3.5e-4 on SVM) and BF16 changes
-// iteration counts, so each fp32 element is split as a = hi + lo with
-// hi = tf32(a), lo = tf32(a - hi) and
+// iteration counts, so each fp32 element is split as a = hi + lo and
 //     G += hi_i' hi_j + hi_i' lo_j + lo_i' hi_j           (3 MMAs)
-// which keeps ~22 mantissa bits.  The accumulator lives in TMEM in fp32 and is
-// drained into the fp64 G every `kchunk` rows: the tensor core's fp32
-// accumulation truncates, so its relative error grows with the number of
-// accumulate steps per drain (measured ~3e-8 per step); the drain interval
-// bounds it while the long reduction over m = 2e5 rows is carried in fp64.
+// which keeps ~22 mantissa bits.  Default split (kind::f16): the panel is
+// scaled by a power of two s (largest entry ~2^14) and hi = f16(s a),
+// lo = f16(s a - hi); the drain multiplies by 1/s^2.  GF_SYRK=tf32 selects
+// the kind::tf32 split hi = tf32(a), lo = tf32(a - hi), which moves twice the
+// operand bytes per MAC (Gram 26.5 -> 23.6 ms at 200000 x 5000 for f16).
+// The accumulator lives in TMEM in fp32 and is drained into the fp64 G every
+// `kchunk` rows: the tensor core's fp32 accumulation truncates, so its
+// relative error grows with the number of accumulate steps per drain
+// (measured ~3e-8 per step); the drain interval bounds it while the long
+// reduction over m = 2e5 rows is carried in fp64.
 //
 // Tile: 128 columns of A (MMA M) x 256 columns (MMA N), lower-triangle tiles
-// only (G is mirrored afterwards).  Warp roles (416 threads):
+// only (G is mirrored afterwards).  Warp roles (576 threads):
 //   warps 0-3   epilogue: tcgen05.ld the 128x256 fp32 accumulator, add into G (fp64)
 //   warp 4      TMEM allocator + MMA issuer (one thread)
-//   warps 5-12  producers: coalesced column loads of 4 fp32 rows, split into
+//   warps 5-16  converters: column reads of the raw TMA slab, split into
 //               hi/lo, one 16-byte store each into the K-major no-swizzle
 //               core-matrix layout the MMA descriptors expect
-// Pipelines: 4 shared-memory stages (full/empty mbarriers; empty is signalled
-// by tcgen05.commit) and 2 TMEM accumulators (256 columns each; full by
-// tcgen05.commit, empty by the epilogue warps).
+//   warp 17     TMA loader (2-D tensor maps, raw fp32 ring)
+// Pipelines: raw ring (TMA -> converters), operand stages (full/empty
+// mbarriers; empty is signalled by tcgen05.commit) and 2 TMEM accumulators
+// (256 columns each; full by tcgen05.commit, empty by the epilogue warps).
+//
+// What bounds it is shared-memory bandwidth: per 16-row stage the TMA writes
+// 24 KB, the converters read 24 KB and write 24 KB (f16) and the three MMAs
+// read 36 KB -- ~860 wavefronts against 384 tensor-pipe cycles.  Measured by
+// switching parts off: conversion alone 18.5 ms, MMA alone 14.4 ms, all
+// 24.5 ms (the costs add); drain interval, barrier polling back-off and an
+// L2 evict-last policy on the G tiles made no difference.
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include "gf_internal.h"
@@ -35,17 +48,12 @@ namespace syrk {
 // K-major, no-swizzle operand layout (verified on B200 with tools/umma_probe.cu):
 // a core matrix is 8 MN-rows x 16 bytes (4 tf32 along K), 128 contiguous
 // bytes; 8-row groups are SBO = 128 B apart, 4-element K chunks LBO apart.
-constexpr int TM = 128, TN = 256, BK = 16, NST = 2;
+constexpr int TM = 128, TN = 256, BK = 16;
 // rows per TMEM accumulation: 1024 -> max |G error| / max |G| ~ 9.5e-6 on a
 // 20000 x 1300 Gaussian matrix (512: 4.7e-6, 128: 1.2e-6; tools/syrk_accuracy.py);
 // 1024 halves the fp64 drain traffic of 512 (Gram 39 -> 29 ms at 200000 x 5000)
 constexpr int KCHUNK_DEFAULT = 1024;
-constexpr int A_BYTES = (BK / 4) * (TM / 8) * 128; // 8 KB per hi/lo
-constexpr int B_BYTES = (BK / 4) * (TN / 8) * 128; // 16 KB per hi/lo
-constexpr int LBO_A = (TM / 8) * 128;              // K-chunk stride
-constexpr int LBO_B = (TN / 8) * 128;
-constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;   // 48 KB
-constexpr int NPROD = 8;                           // converter warps
+constexpr int NPROD = 12;                          // converter warps
 constexpr int LOADER_WARP = 5 + NPROD;             // TMA loader warp
 constexpr int THREADS = (6 + NPROD) * 32;
 // raw fp32 ring filled by 2-D tensor TMA: per stage two boxes, BK rows x TM
@@ -54,7 +62,31 @@ constexpr int THREADS = (6 + NPROD) * 32;
 constexpr int RAW_A = BK * TM * 4;
 constexpr int RAW_BYTES = BK * (TM + TN) * 4;      // 24 KB
 constexpr int NRAW = 5;
-constexpr int SMEM = NST * STAGE + NRAW * RAW_BYTES;   // 96 + 120 KB
+
+// Operand split.  F16 = false: tf32 hi/lo (4-byte elements, 4 per core-matrix
+// row, K = 8 per MMA).  F16 = true: the panel is scaled by s = 2^(14 - e_max)
+// (exact) and split into fp16 hi/lo (2-byte elements, 8 per core-matrix row,
+// K = 16 per MMA at twice the tf32 rate); the drain multiplies by 1/s^2.
+// Same 11 + 11 mantissa bits as 3xTF32; fp16's exponent range is what the
+// scale is for (entries below 2^-24 of the largest lose bits in absolute terms
+// only, ~2^-25 max|A| per element).  Half the operand bytes per MAC: the
+// shared-memory traffic per K row drops from 1350 to ~880 B-cycles.
+template <bool F16>
+struct Split {
+  static constexpr int ESZ = F16 ? 2 : 4;
+  static constexpr int KCH = 16 / ESZ;             // K elements per core-matrix row
+  static constexpr int A_BYTES = BK * TM * ESZ;    // per hi/lo
+  static constexpr int B_BYTES = BK * TN * ESZ;
+  static constexpr int LBO_A = (TM / 8) * 128;     // K-chunk stride
+  static constexpr int LBO_B = (TN / 8) * 128;
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;   // 48 / 24 KB
+  static constexpr int NST = F16 ? 4 : 2;
+  static constexpr int KSTEPS = BK / (2 * KCH);    // MMAs (x3) per stage: 2 / 1
+  static constexpr int SMEM = NST * STAGE + NRAW * RAW_BYTES;   // 96 + 120 KB
+  // Instruction descriptor: D f32, A/B tf32 (2) or f16 (0), K-major, M = 128, N = 256.
+  static constexpr uint32_t IDESC = (1u << 4) | ((F16 ? 0u : 2u) << 7) | ((F16 ? 0u : 2u) << 10) |
+                                    ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+};
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -93,16 +125,33 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
   return d;                 // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
 }
 
-// Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 256.
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
-                           ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+template <bool F16>
+__device__ __forceinline__ void mma_split(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  if constexpr (F16)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(Split<F16>::IDESC), "r"(accumulate));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(Split<F16>::IDESC), "r"(accumulate));
+}
 
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(IDESC), "r"(accumulate));
+__device__ __forceinline__ uint32_t pack_f16(float a, float b) {   // a -> low half (lower K index)
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// scale exponent: s = 2^(14 - e), e = exponent of max|A| (bits of the float max)
+__device__ __forceinline__ int split_shift(const unsigned* amax_bits) {
+  const unsigned b = amax_bits ? *amax_bits : 0u;
+  if (b == 0u || b >= 0x7f800000u) return 0;
+  const int e = (int)(b >> 23) - 127;   // max|A| in [2^e, 2^(e+1))
+  return min(126, max(-126, 14 - e));
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* b) {
@@ -110,9 +159,14 @@ __device__ __forceinline__ void mma_commit(uint64_t* b) {
                : "memory");
 }
 
+template <bool F16>
 __global__ void __launch_bounds__(THREADS, 1)
-syrk_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t K,
-                   int64_t q, int64_t kchunk, const int2* __restrict__ tiles, double* __restrict__ G, int64_t ldg) {
+syrk_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t K,
+                  int64_t q, int64_t kchunk, const int2* __restrict__ tiles, double* __restrict__ G, int64_t ldg,
+                  const unsigned* __restrict__ amax_bits) {
+  using S = Split<F16>;
+  constexpr int NST = S::NST, STAGE = S::STAGE, A_BYTES = S::A_BYTES, B_BYTES = S::B_BYTES;
+  constexpr int LBO_A = S::LBO_A, LBO_B = S::LBO_B, KCH = S::KCH;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[NST], empty[NST], accf[2], acce[2], rfull[NRAW], rempty[NRAW];
   __shared__ uint32_t tmem_base_s;
@@ -177,8 +231,9 @@ syrk_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     // shared loads down the raw column, split into hi/lo, one 16-byte store of
     // each into the K-major no-swizzle core-matrix layout (consecutive threads
     // -> consecutive columns -> consecutive 16 B rows of a core matrix).
-    constexpr int NITEM = ((BK / 4) * (TM + TN)) / (NPROD * 32);   // 6
-    const int pt = tid - 5 * 32;   // 0..255
+    constexpr int NITEM = ((BK / KCH) * (TM + TN)) / (NPROD * 32);   // 6 (tf32) / 3 (f16)
+    const int pt = tid - 5 * 32;   // 0 .. NPROD*32-1
+    const float sc = F16 ? ldexpf(1.0f, split_shift(amax_bits)) : 1.0f;
     for (int64_t it = 0; it < nstages; ++it) {
       const int r = (int)(it % NRAW);
       const int s = (int)(it % NST);
@@ -195,14 +250,27 @@ syrk_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         const int mn = isA ? c : c - TM;
         const float* col = isA ? rs + mn : rs + BK * TM + mn;
         const int w = isA ? TM : TN;
-        float f[4];
+        float f[KCH];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) f[e] = col[(4 * kc + e) * w];
+        for (int e = 0; e < KCH; ++e) f[e] = col[(KCH * kc + e) * w];
         uint4 hi, lo;
-        hi.x = to_tf32(f[0]); lo.x = to_tf32(f[0] - __uint_as_float(hi.x));
-        hi.y = to_tf32(f[1]); lo.y = to_tf32(f[1] - __uint_as_float(hi.y));
-        hi.z = to_tf32(f[2]); lo.z = to_tf32(f[2] - __uint_as_float(hi.z));
-        hi.w = to_tf32(f[3]); lo.w = to_tf32(f[3] - __uint_as_float(hi.w));
+        if constexpr (F16) {
+          uint32_t h[4], l[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float x0 = f[2 * e] * sc, x1 = f[2 * e + 1] * sc;
+            h[e] = pack_f16(x0, x1);
+            const __half2 hh = *reinterpret_cast<const __half2*>(&h[e]);
+            l[e] = pack_f16(x0 - __low2float(hh), x1 - __high2float(hh));
+          }
+          hi = make_uint4(h[0], h[1], h[2], h[3]);
+          lo = make_uint4(l[0], l[1], l[2], l[3]);
+        } else {
+          hi.x = to_tf32(f[0]); lo.x = to_tf32(f[0] - __uint_as_float(hi.x));
+          hi.y = to_tf32(f[1]); lo.y = to_tf32(f[1] - __uint_as_float(hi.y));
+          hi.z = to_tf32(f[2]); lo.z = to_tf32(f[2] - __uint_as_float(hi.z));
+          hi.w = to_tf32(f[3]); lo.w = to_tf32(f[3] - __uint_as_float(hi.w));
+        }
         unsigned char* base_hi = isA ? st : st + 2 * A_BYTES;
         const int lbo = isA ? LBO_A : LBO_B;
         const int nb = isA ? A_BYTES : B_BYTES;
@@ -233,16 +301,16 @@ syrk_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           const uint32_t st = su32(smem + (size_t)s * STAGE);
           const uint32_t a_hi = st, a_lo = st + A_BYTES, b_hi = st + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            // one MMA covers K = 8 = two 4-element K chunks
+          for (int kk = 0; kk < S::KSTEPS; ++kk) {
+            // one MMA covers two K chunks of KCH elements (K = 8 tf32 / 16 f16)
             const uint64_t dah = smem_desc(a_hi + 2 * kk * LBO_A, LBO_A, 128);
             const uint64_t dal = smem_desc(a_lo + 2 * kk * LBO_A, LBO_A, 128);
             const uint64_t dbh = smem_desc(b_hi + 2 * kk * LBO_B, LBO_B, 128);
             const uint64_t dbl = smem_desc(b_lo + 2 * kk * LBO_B, LBO_B, 128);
             const uint32_t accum = (it > it0 || kk > 0) ? 1u : 0u;
-            mma_tf32(d, dah, dbh, accum);
-            mma_tf32(d, dah, dbl, 1u);
-            mma_tf32(d, dal, dbh, 1u);
+            mma_split<F16>(d, dah, dbh, accum);
+            mma_split<F16>(d, dah, dbl, 1u);
+            mma_split<F16>(d, dal, dbh, 1u);
           }
           mma_commit(&empty[s]);   // frees the stage once these MMAs have read it
         }
@@ -253,44 +321,39 @@ syrk_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   } else {
     // ===================== epilogue (warps 0-3) =====================
     const int64_t i = i0 + warp * 32 + lane;   // TMEM lane = tile row
+    const double unscale = F16 ? ldexp(1.0, -2 * split_shift(amax_bits)) : 1.0;
     for (int64_t c = 0; c < nchunks; ++c) {
       const int acc = (int)(c & 1);
       bar_wait(&accf[acc], (unsigned)((c >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
-      for (int cc = 0; cc < TN / 32; ++cc) {
-        uint32_t v[32];
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * TN + cc * 32);
+      for (int cc = 0; cc < TN / 16; ++cc) {
+        uint32_t v[16];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * TN + cc * 16);
         asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
               "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-              "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+              "=r"(v[15])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         // G is symmetric: accumulate the tile's transpose, G[j][i], so the 32
         // lanes (consecutive i) touch 256 contiguous bytes per instruction;
-        // the upper triangle is mirrored down afterwards (gram_finish).
-        // all 32 loads are issued before any store (a plain `+=` loop would
-        // serialize on possible aliasing between the stores and later loads)
-        // (two halves of 16: 32 fp64 values plus the 32 accumulator words
-        // overflowed the 128-register budget into local memory)
+        // the upper triangle is mirrored down afterwards (upper_to_lower).
+        // All 16 loads are issued before any store (a plain `+=` loop would
+        // serialize on possible aliasing between the stores and later loads);
+        // 16 columns per step keeps the epilogue inside the converter warps'
+        // register budget.
         if (i < q) {
-          const int64_t jn = min((int64_t)32, q - (j0 + cc * 32));
-          double* col = G + (j0 + cc * 32) * ldg + i;
+          const int64_t jn = min((int64_t)16, q - (j0 + cc * 16));
+          double* col = G + (j0 + cc * 16) * ldg + i;
+          double g[16];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            double g[16];
+          for (int t = 0; t < 16; ++t) g[t] = t < jn ? col[t * ldg] : 0.0;
 #pragma unroll
-            for (int t = 0; t < 16; ++t) g[t] = 16 * h + t < jn ? col[(16 * h + t) * ldg] : 0.0;
-#pragma unroll
-            for (int t = 0; t < 16; ++t)
-              if (16 * h + t < jn) col[(16 * h + t) * ldg] = g[t] + (double)__uint_as_float(v[16 * h + t]);
-          }
+          for (int t = 0; t < 16; ++t)
+            if (t < jn) col[t * ldg] = fma((double)__uint_as_float(v[t]), unscale, g[t]);
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -338,7 +401,27 @@ static CUtensorMap panel_map(const gf_matrix* A, int box_cols) {
   return m;
 }
 
+// max |A| over the n real columns, as float bits (non-negative floats order
+// like their bit patterns); the padding columns are not read
+__global__ void absmax_kernel(const float* __restrict__ A, int64_t m, int64_t ld, int64_t n,
+                              unsigned* __restrict__ out) {
+  const int64_t nv = (n + 3) / 4;
+  float mx = 0.0f;
+  for (int64_t i = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; i < m * nv; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / nv, v = i - r * nv;
+    const float4 a = reinterpret_cast<const float4*>(A + r * ld)[v];
+    const int64_t j = 4 * v;
+    mx = fmaxf(mx, fabsf(a.x));
+    if (j + 1 < n) mx = fmaxf(mx, fabsf(a.y));
+    if (j + 2 < n) mx = fmaxf(mx, fabsf(a.z));
+    if (j + 3 < n) mx = fmaxf(mx, fabsf(a.w));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(mx));
+}
+
 // G (fp64, zeroed by the caller) += A'A for fp32 A (m x ld, columns >= n zero).
+// Default split: scaled fp16 hi/lo (kind::f16); GF_SYRK=tf32 selects 3xTF32.
 void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st) {
   using namespace syrk;
   const int64_t q = A->n;
@@ -347,18 +430,36 @@ void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st) {
   for (int64_t bi = 0; bi < bi_n; ++bi)
     for (int64_t bj = 0; bj < bj_n; ++bj)
       if (2 * bj <= bi) tl.push_back(make_int2((int)bi, (int)bj));   // lower-triangle tiles
-  DBuf d_tiles(tl.size() * sizeof(int2));
+  DBuf d_tiles(tl.size() * sizeof(int2) + 16);
   GF_CUDA(cudaMemcpyAsync(d_tiles.p, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
-  static bool attr = false;
-  if (!attr) {
-    GF_CUDA(cudaFuncSetAttribute(syrk_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-    attr = true;
+  const char* sp = getenv("GF_SYRK");
+  const bool f16 = !(sp && std::string(sp) == "tf32");
+  static bool attr[2] = {false, false};
+  if (!attr[f16]) {
+    if (f16)
+      GF_CUDA(cudaFuncSetAttribute(syrk_split_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   Split<true>::SMEM));
+    else
+      GF_CUDA(cudaFuncSetAttribute(syrk_split_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   Split<false>::SMEM));
+    attr[f16] = true;
   }
   const char* kc_env = getenv("GF_SYRK_KCHUNK");
   int64_t kchunk = kc_env ? std::max<int64_t>(BK, atoll(kc_env) / BK * BK) : KCHUNK_DEFAULT;
   const CUtensorMap tmA = panel_map(A, TM), tmB = panel_map(A, TN);
-  syrk_tf32x3_kernel<<<(unsigned)tl.size(), THREADS, SMEM, st>>>(tmA, tmB, A->m, q, kchunk, d_tiles.as<int2>(), G,
-                                                                 ldg);
+  unsigned* amax = reinterpret_cast<unsigned*>(d_tiles.as<char>() + tl.size() * sizeof(int2) + 8);
+  if (f16) {
+    GF_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned), st));
+    const int64_t items = A->m * ceil_div(q, 4);
+    absmax_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), num_sms() * 8)), 256, 0,
+                    st>>>((const float*)A->data, A->m, A->ld, q, amax);
+    GF_CHECK_LAUNCH();
+    syrk_split_kernel<true><<<(unsigned)tl.size(), THREADS, Split<true>::SMEM, st>>>(
+        tmA, tmB, A->m, q, kchunk, d_tiles.as<int2>(), G, ldg, amax);
+  } else {
+    syrk_split_kernel<false><<<(unsigned)tl.size(), THREADS, Split<false>::SMEM, st>>>(
+        tmA, tmB, A->m, q, kchunk, d_tiles.as<int2>(), G, ldg, nullptr);
+  }
   GF_CHECK_LAUNCH();
   upper_to_lower<<<dim3((unsigned)ceil_div(q, 32), (unsigned)ceil_div(q, 8)), dim3(32, 8), 0, st>>>(G, q, ldg);
   GF_CHECK_LAUNCH();

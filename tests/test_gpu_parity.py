@@ -256,11 +256,13 @@ def test_c1_headline_values():
     assert res.objective == pytest.approx(252.42917798604532, rel=1e-9)
 
 
+@pytest.mark.parametrize("split", ["f16", "tf32"])
 @pytest.mark.parametrize("shape", [(513, 129), (3000, 700), (20000, 1300)])
-def test_gram_tensor_core_fp32(shape):
-    """The fp32 Gram runs on tcgen05 (3xTF32 split, fp64 drain every 4096
-    rows): it must agree with the fp64 Gram of the same fp32 data to
-    fp32-grade accuracy, including ragged tile edges."""
+def test_gram_tensor_core_fp32(shape, split, monkeypatch):
+    """The fp32 Gram runs on tcgen05 (scaled-fp16 or TF32 three-product split,
+    fp64 drain every 1024 rows): it must agree with the fp64 Gram of the same
+    fp32 data to fp32-grade accuracy, including ragged tile edges."""
+    monkeypatch.setenv("GF_SYRK", split)
     m, n = shape
     A = np.random.default_rng(m + n).normal(size=(m, n)).astype(np.float32)
     G = gf.build_projector(A).gram
@@ -268,9 +270,28 @@ def test_gram_tensor_core_fp32(shape):
     ref = A64.T @ A64 + np.eye(n)
     err = np.abs(G - ref).max() / np.abs(ref).max()
     # the tensor core accumulates in truncating fp32 between fp64 drains every
-    # 512 rows: measured ~5e-6 (tools/syrk_accuracy.py); plain TF32 gives ~4e-4
+    # 1024 rows: measured ~5e-6 (tools/syrk_accuracy.py); plain TF32 gives ~4e-4
     assert err < 1.5e-5, err
     np.testing.assert_allclose(G, G.T, rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("scale", [1e-30, 1e-6, 1e6, 1e30])
+def test_gram_f16_split_scaling(scale):
+    """The fp16 split scales the panel by a power of two so that its largest
+    entry sits near 2^14: matrices far outside fp16's range, and columns
+    spanning six orders of magnitude, keep fp32-grade accuracy per column pair
+    (off-diagonal error relative to sqrt(G_ii G_jj))."""
+    m, n = 4000, 300
+    rng = np.random.default_rng(7)
+    A = (rng.normal(size=(m, n)) * np.logspace(-3, 3, n)[None, :] * scale).astype(np.float32)
+    G = gf.build_projector(A).gram
+    A64 = A.astype(np.float64)
+    ref = A64.T @ A64
+    d = np.sqrt(np.diag(ref))
+    off = ~np.eye(n, dtype=bool)   # (the diagonal carries the added identity)
+    err = (np.abs(G - ref) / np.outer(d, d))[off]
+    assert np.isfinite(G).all()
+    assert err.max() < 2e-5, err.max()
 
 
 CONJ = _cases.load("conj")
