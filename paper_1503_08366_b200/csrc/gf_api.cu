@@ -101,17 +101,17 @@ static ScratchArena& arena_for_current_device() {
 struct ScratchLock {
   ScratchArena& a;
   std::lock_guard<std::mutex> lk;
-  ScratchLock(int count, size_t bytes) : a(arena_for_current_device()), lk(a.mu) {
-    for (int i = 0; i < count; ++i)
-      if (a.bytes[i] < bytes) {
-        if (a.p[i]) GF_CUDA(cudaFree(a.p[i]));
-        a.p[i] = nullptr;
-        a.bytes[i] = 0;
-        GF_CUDA(cudaMalloc(&a.p[i], bytes));
-        a.bytes[i] = bytes;
-      }
+  ScratchLock() : a(arena_for_current_device()), lk(a.mu) {}
+  void* get(int i, size_t bytes) {   // slot i, grown to at least `bytes`
+    if (a.bytes[i] < bytes) {
+      if (a.p[i]) GF_CUDA(cudaFree(a.p[i]));
+      a.p[i] = nullptr;
+      a.bytes[i] = 0;
+      GF_CUDA(cudaMalloc(&a.p[i], bytes));
+      a.bytes[i] = bytes;
+    }
+    return a.p[i];
   }
-  void* ptr(int i) const { return a.p[i]; }
 };
 struct DBufView {
   void* p;
@@ -241,15 +241,25 @@ static gf_projector* projector_build(gf_matrix* A, int mode, double tol, int64_t
   P->gram.alloc(gbytes);
   GF_CUDA(cudaMemsetAsync(P->gram.p, 0, gbytes, st));
   PhaseTimer pt(st);
-  if (A->m > 0 && A->n > 0) gram_accumulate(A, P->tall, P->gram.as<double>(), P->ldg, st);
+  // large temporaries come from a grow-only per-device arena: growing the
+  // stream-ordered pool by hundreds of MB mid-setup was measured to stall the
+  // host for 10-250 ms on some boxes (slot 3: the Gram's pre-split copy of A,
+  // used when it fits -- or already fits -- with 1 GB to spare)
+  ScratchLock sl;
+  void* gscratch = nullptr;
+  size_t gsb = A->m > 0 && A->n > 0 ? gram_scratch_bytes(A, P->tall) : 0;
+  if (gsb > 0 && sl.a.bytes[3] < gsb) {
+    size_t free_b = 0, total_b = 0;
+    GF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (gsb - sl.a.bytes[3] + (1ull << 30) >= free_b) gsb = 0;
+  }
+  if (gsb > 0) gscratch = sl.get(3, gsb);
+  if (A->m > 0 && A->n > 0) gram_accumulate(A, P->tall, P->gram.as<double>(), P->ldg, st, gscratch, gsb);
   if (comm_active(comm)) allreduce_sum(comm, P->gram.as<double>(), (size_t)q * P->ldg, st);
   gram_finish(P->gram.as<double>(), q, P->ldg, st);
   pt.mark("gram");
-  // the three q x q fp64 temporaries come from a grow-only per-device arena:
-  // growing the stream-ordered pool by hundreds of MB mid-setup was measured
-  // to stall the host for 10-250 ms on some boxes
-  ScratchLock sl(3, gbytes);
-  DBufView L(sl.ptr(0)), tmp(sl.ptr(1)), inv(sl.ptr(2));
+  // the three q x q fp64 temporaries (arena slots 0-2)
+  DBufView L(sl.get(0, gbytes)), tmp(sl.get(1, gbytes)), inv(sl.get(2, gbytes));
   DBuf info(sizeof(int));
   GF_CUDA(cudaMemcpyAsync(L.p, P->gram.p, gbytes, cudaMemcpyDeviceToDevice, st));
   const int bad = cholesky(L.as<double>(), q, P->ldg, info.as<int>(), st);

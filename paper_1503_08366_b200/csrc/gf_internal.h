@@ -66,8 +66,13 @@ struct DBuf {
 };
 
 // ------------------------------------------------ dense setup (gf_dense) --
-void gram_accumulate(const gf_matrix* A, bool tall, double* G, int64_t ldg, cudaStream_t st);
-void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st);  // tcgen05, G += A'A
+// Gram scratch: bytes of the pre-split fp16 copy gram_tf32x3 can use for A
+// (0 when the f16 pre-split path does not apply); `scratch` may be null.
+size_t gram_scratch_bytes(const gf_matrix* A, bool tall);
+void gram_accumulate(const gf_matrix* A, bool tall, double* G, int64_t ldg, cudaStream_t st,
+                     void* scratch = nullptr, size_t scratch_bytes = 0);
+void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, void* scratch = nullptr,
+                 size_t scratch_bytes = 0);  // tcgen05, G += A'A
 void gram_finish(double* G, int64_t q, int64_t ldg, cudaStream_t st);
 int cholesky(double* G, int64_t q, int64_t ld, int* d_info, cudaStream_t st);
 void trtri(double* L, int64_t q, int64_t ld, double* tmp, cudaStream_t st);

@@ -37,6 +37,7 @@
 // L2 evict-last policy on the G tiles made no difference.
 
 #include <cuda.h>
+#include <chrono>
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
@@ -157,6 +158,42 @@ __device__ __forceinline__ int split_shift(const unsigned* amax_bits) {
 __device__ __forceinline__ void mma_commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b))
                : "memory");
+}
+
+// Epilogue warp `warp` (0-3) adds its 32 TMEM lanes (tile rows i) of
+// accumulator `acc` into G, scaled by `unscale`.
+__device__ __forceinline__ void drain_chunk(uint32_t tmem, int warp, int acc, int64_t i, int64_t j0, int64_t q,
+                                            double* __restrict__ G, int64_t ldg, double unscale) {
+#pragma unroll 1
+  for (int cc = 0; cc < TN / 16; ++cc) {
+    uint32_t v[16];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * TN + cc * 16);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+          "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    // G is symmetric: accumulate the tile's transpose, G[j][i], so the 32
+    // lanes (consecutive i) touch 256 contiguous bytes per instruction;
+    // the upper triangle is mirrored down afterwards (upper_to_lower).
+    // All 16 loads are issued before any store (a plain `+=` loop would
+    // serialize on possible aliasing between the stores and later loads);
+    // 16 columns per step keeps the epilogue inside the converter warps'
+    // register budget.
+    if (i < q) {
+      const int64_t jn = min((int64_t)16, q - (j0 + cc * 16));
+      double* col = G + (j0 + cc * 16) * ldg + i;
+      double g[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) g[t] = t < jn ? col[t * ldg] : 0.0;
+#pragma unroll
+      for (int t = 0; t < 16; ++t)
+        if (t < jn) col[t * ldg] = fma((double)__uint_as_float(v[t]), unscale, g[t]);
+    }
+  }
 }
 
 template <bool F16>
@@ -326,36 +363,160 @@ syrk_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
       const int acc = (int)(c & 1);
       bar_wait(&accf[acc], (unsigned)((c >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll 1
-      for (int cc = 0; cc < TN / 16; ++cc) {
-        uint32_t v[16];
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * TN + cc * 16);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-              "=r"(v[15])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        // G is symmetric: accumulate the tile's transpose, G[j][i], so the 32
-        // lanes (consecutive i) touch 256 contiguous bytes per instruction;
-        // the upper triangle is mirrored down afterwards (upper_to_lower).
-        // All 16 loads are issued before any store (a plain `+=` loop would
-        // serialize on possible aliasing between the stores and later loads);
-        // 16 columns per step keeps the epilogue inside the converter warps'
-        // register budget.
-        if (i < q) {
-          const int64_t jn = min((int64_t)16, q - (j0 + cc * 16));
-          double* col = G + (j0 + cc * 16) * ldg + i;
-          double g[16];
+      drain_chunk(tmem, warp, acc, i, j0, q, G, ldg, unscale);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) bar_arrive(&acce[acc]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// ---- pre-split variant -------------------------------------------------
+// The converters above split every panel once per tile that reads it (~20x
+// for q = 5000), and their shared-memory traffic is what bounds the kernel.
+// When there is room for a second copy of A (4 bytes per element), one
+// streaming pass writes hi/lo once, already in the MMA's K-major core-matrix
+// order: element (r, c) at [(r / 8) * ncp + c] * 8 + r % 8 (fp16), zero past
+// the matrix.  The Gram kernel then only moves bytes: bulk copies straight
+// into the operand stages, three MMAs per stage, no conversion warps.
+__global__ void __launch_bounds__(256) split_f16_kernel(const float* __restrict__ A, int64_t m, int64_t ld, int64_t n,
+                                                        int64_t ncp, int64_t nkb,
+                                                        const unsigned* __restrict__ amax_bits,
+                                                        uint4* __restrict__ hi, uint4* __restrict__ lo) {
+  const float sc = ldexpf(1.0f, split_shift(amax_bits));
+  for (int64_t idx = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; idx < nkb * ncp;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t kb = idx / ncp, c = idx - kb * ncp;
+    float f[8];
 #pragma unroll
-          for (int t = 0; t < 16; ++t) g[t] = t < jn ? col[t * ldg] : 0.0;
+    for (int e = 0; e < 8; ++e) {
+      const int64_t r = kb * 8 + e;
+      f[e] = (r < m && c < n) ? A[r * ld + c] : 0.0f;
+    }
+    uint32_t h[4], l[4];
 #pragma unroll
-          for (int t = 0; t < 16; ++t)
-            if (t < jn) col[t * ldg] = fma((double)__uint_as_float(v[t]), unscale, g[t]);
+    for (int e = 0; e < 4; ++e) {
+      const float x0 = f[2 * e] * sc, x1 = f[2 * e + 1] * sc;
+      h[e] = pack_f16(x0, x1);
+      const __half2 hh = *reinterpret_cast<const __half2*>(&h[e]);
+      l[e] = pack_f16(x0 - __low2float(hh), x1 - __high2float(hh));
+    }
+    hi[idx] = make_uint4(h[0], h[1], h[2], h[3]);
+    lo[idx] = make_uint4(l[0], l[1], l[2], l[3]);
+  }
+}
+
+constexpr int PRE_NST = 8;                                  // 8 x 24 KB operand stages
+constexpr int PRE_THREADS = 6 * 32;                         // epilogue 0-3, MMA 4, loader 5
+constexpr int PRE_SMEM = PRE_NST * Split<true>::STAGE;
+
+__global__ void __launch_bounds__(PRE_THREADS, 1)
+syrk_pre_kernel(const unsigned char* __restrict__ hi, const unsigned char* __restrict__ lo, int64_t ncp, int64_t nkb,
+                int64_t q, int64_t kchunk, const int2* __restrict__ tiles, double* __restrict__ G, int64_t ldg,
+                const unsigned* __restrict__ amax_bits) {
+  using S = Split<true>;
+  constexpr int STAGE = S::STAGE, A_BYTES = S::A_BYTES, B_BYTES = S::B_BYTES, LBO_A = S::LBO_A, LBO_B = S::LBO_B;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[PRE_NST], empty[PRE_NST], accf[2], acce[2];
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int2 tile = tiles[blockIdx.x];
+  const int64_t i0 = (int64_t)tile.x * TM, j0 = (int64_t)tile.y * TN;
+  const int64_t nstages = nkb / 2;                          // 16 rows per stage
+  const int64_t nchunks = (nstages * BK + kchunk - 1) / kchunk;
+  const int64_t SPC = kchunk / BK;
+
+  if (tid == 0) {
+    for (int s = 0; s < PRE_NST; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      bar_init(&accf[a], 1);
+      bar_init(&acce[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base_s)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 5) {
+    // ===================== loader: 8 bulk copies per stage =====================
+    if (lane == 0) {
+      const int64_t row_bytes = ncp * 16;                   // one 8-row block, all columns
+      for (int64_t it = 0; it < nstages; ++it) {
+        const int s = (int)(it % PRE_NST);
+        if (it >= PRE_NST) bar_wait(&empty[s], (unsigned)(((it / PRE_NST) - 1) & 1));
+        const uint32_t st = su32(smem + (size_t)s * STAGE), bar = su32(&full[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)STAGE)
+                     : "memory");
+#pragma unroll
+        for (int kc = 0; kc < 2; ++kc) {
+          const int64_t kb = 2 * it + kc;
+          const unsigned char* srcs[2] = {hi, lo};
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+            const unsigned char* base = srcs[part] + kb * row_bytes;
+            const uint32_t da = st + part * A_BYTES + kc * LBO_A;
+            const uint32_t db = st + 2 * A_BYTES + part * B_BYTES + kc * LBO_B;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(da),
+                "l"(base + i0 * 16), "r"((unsigned)(TM * 16)), "r"(bar)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(db),
+                "l"(base + j0 * 16), "r"((unsigned)(TN * 16)), "r"(bar)
+                : "memory");
+          }
         }
       }
+    }
+  } else if (warp == 4) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      for (int64_t c = 0; c < nchunks; ++c) {
+        const int acc = (int)(c & 1);
+        if (c >= 2) bar_wait(&acce[acc], (unsigned)(((c >> 1) - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + (uint32_t)(acc * TN);
+        const int64_t it0 = c * SPC, it1 = min(nstages, it0 + SPC);
+        for (int64_t it = it0; it < it1; ++it) {
+          const int s = (int)(it % PRE_NST);
+          bar_wait(&full[s], (unsigned)((it / PRE_NST) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t st = su32(smem + (size_t)s * STAGE);
+          const uint32_t a_hi = st, a_lo = st + A_BYTES, b_hi = st + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
+          const uint64_t dah = smem_desc(a_hi, LBO_A, 128), dal = smem_desc(a_lo, LBO_A, 128);
+          const uint64_t dbh = smem_desc(b_hi, LBO_B, 128), dbl = smem_desc(b_lo, LBO_B, 128);
+          mma_split<true>(d, dah, dbh, it > it0 ? 1u : 0u);
+          mma_split<true>(d, dah, dbl, 1u);
+          mma_split<true>(d, dal, dbh, 1u);
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&accf[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== epilogue (warps 0-3) =====================
+    const int64_t i = i0 + warp * 32 + lane;
+    const double unscale = ldexp(1.0, -2 * split_shift(amax_bits));
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int acc = (int)(c & 1);
+      bar_wait(&accf[acc], (unsigned)((c >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      drain_chunk(tmem, warp, acc, i, j0, q, G, ldg, unscale);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) bar_arrive(&acce[acc]);
@@ -401,6 +562,13 @@ static CUtensorMap panel_map(const gf_matrix* A, int box_cols) {
   return m;
 }
 
+size_t gram_scratch_bytes(const gf_matrix* A, bool tall) {
+  const char* sp = getenv("GF_SYRK");   // "tf32" / "f16": the in-kernel converters, no copy
+  if (!tall || A->dtype != GF_F32 || (sp && (std::string(sp) == "tf32" || std::string(sp) == "f16"))) return 0;
+  const int64_t ncp = ceil_div(A->n, syrk::TN) * syrk::TN, nkb = ceil_div(A->m, syrk::BK) * 2;
+  return 2 * (size_t)nkb * ncp * 16;
+}
+
 // max |A| over the n real columns, as float bits (non-negative floats order
 // like their bit patterns); the padding columns are not read
 __global__ void absmax_kernel(const float* __restrict__ A, int64_t m, int64_t ld, int64_t n,
@@ -422,7 +590,7 @@ __global__ void absmax_kernel(const float* __restrict__ A, int64_t m, int64_t ld
 
 // G (fp64, zeroed by the caller) += A'A for fp32 A (m x ld, columns >= n zero).
 // Default split: scaled fp16 hi/lo (kind::f16); GF_SYRK=tf32 selects 3xTF32.
-void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st) {
+void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, void* scratch, size_t scratch_bytes) {
   using namespace syrk;
   const int64_t q = A->n;
   const int64_t bi_n = ceil_div(q, TM), bj_n = ceil_div(q, TN);
@@ -434,6 +602,9 @@ void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st) {
   GF_CUDA(cudaMemcpyAsync(d_tiles.p, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
   const char* sp = getenv("GF_SYRK");
   const bool f16 = !(sp && std::string(sp) == "tf32");
+  const int64_t ncp = ceil_div(q, TN) * TN, nkb = ceil_div(A->m, BK) * 2;
+  const size_t pre_bytes = (size_t)nkb * ncp * 16;          // each of hi, lo
+  const bool pre = f16 && scratch != nullptr && scratch_bytes >= 2 * pre_bytes;
   static bool attr[2] = {false, false};
   if (!attr[f16]) {
     if (f16)
@@ -454,8 +625,40 @@ void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st) {
     absmax_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), num_sms() * 8)), 256, 0,
                     st>>>((const float*)A->data, A->m, A->ld, q, amax);
     GF_CHECK_LAUNCH();
-    syrk_split_kernel<true><<<(unsigned)tl.size(), THREADS, Split<true>::SMEM, st>>>(
-        tmA, tmB, A->m, q, kchunk, d_tiles.as<int2>(), G, ldg, amax);
+    if (pre) {
+      static bool pre_attr = false;
+      if (!pre_attr) {
+        GF_CUDA(cudaFuncSetAttribute(syrk_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PRE_SMEM));
+        pre_attr = true;
+      }
+      const char* vb = getenv("GF_VERBOSE_SETUP");
+      const bool verbose = vb && vb[0] == '1';
+      cudaEvent_t ev[3];
+      if (verbose)
+        for (auto& e : ev) GF_CUDA(cudaEventCreate(&e));
+      unsigned char* hi = (unsigned char*)scratch;
+      unsigned char* lo = hi + pre_bytes;
+      if (verbose) GF_CUDA(cudaEventRecord(ev[0], st));
+      split_f16_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nkb * ncp, 256), num_sms() * 16), 256, 0, st>>>(
+          (const float*)A->data, A->m, A->ld, q, ncp, nkb, amax, (uint4*)hi, (uint4*)lo);
+      GF_CHECK_LAUNCH();
+      if (verbose) GF_CUDA(cudaEventRecord(ev[1], st));
+      syrk_pre_kernel<<<(unsigned)tl.size(), PRE_THREADS, PRE_SMEM, st>>>(hi, lo, ncp, nkb, q, kchunk,
+                                                                        d_tiles.as<int2>(), G, ldg, amax);
+      GF_CHECK_LAUNCH();
+      if (verbose) GF_CUDA(cudaEventRecord(ev[2], st));
+      if (verbose) {
+        GF_CUDA(cudaStreamSynchronize(st));
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, ev[0], ev[1]);
+        cudaEventElapsedTime(&b, ev[1], ev[2]);
+        fprintf(stderr, "[gf] gram pre-split: split %.2f ms, syrk %.2f ms\n", a, b);
+        for (auto& e : ev) cudaEventDestroy(e);
+      }
+    } else {
+      syrk_split_kernel<true><<<(unsigned)tl.size(), THREADS, Split<true>::SMEM, st>>>(
+          tmA, tmB, A->m, q, kchunk, d_tiles.as<int2>(), G, ldg, amax);
+    }
   } else {
     syrk_split_kernel<false><<<(unsigned)tl.size(), THREADS, Split<false>::SMEM, st>>>(
         tmA, tmB, A->m, q, kchunk, d_tiles.as<int2>(), G, ldg, nullptr);

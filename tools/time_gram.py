@@ -1,6 +1,6 @@
 """Dev tool: device time of the projector build phases (GF_VERBOSE_SETUP
 lines) for prepare() on the device-drawn bench instance, per Gram split
-(GF_SYRK=f16 default / tf32), a few repetitions each."""
+(GF_SYRK: default pre-split f16 copy / f16 in-kernel converters / tf32), a few repetitions each."""
 import os, sys
 sys.path.insert(0, ".")
 os.environ["GF_VERBOSE_SETUP"] = "1"
@@ -13,8 +13,8 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else 5_000
 prob, _ = instances.tall_lasso(m, n, seed=0, dtype=np.float32, device=True)
 torch.cuda.synchronize()
 ref = None
-for split in ("f16", "tf32", "f16", "tf32"):
-    os.environ["GF_SYRK"] = split
+for split in sys.argv[3].split(",") if len(sys.argv) > 3 else ("pre", "f16", "tf32", "pre", "f16", "tf32"):
+    os.environ["GF_SYRK"] = split   # "pre" (any other value): pre-split copy when it fits
     print("split", split, flush=True)
     S = gf.prepare(prob)
     G = np.array(S.projector.gram)
