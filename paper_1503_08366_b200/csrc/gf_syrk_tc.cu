@@ -414,18 +414,30 @@ constexpr int PRE_NST = 8;                                  // 8 x 24 KB operand
 constexpr int PRE_THREADS = 6 * 32;                         // epilogue 0-3, MMA 4, loader 5
 constexpr int PRE_SMEM = PRE_NST * Split<true>::STAGE;
 
+// CL = 2: a cluster of two CTAs computes tiles (I, J) and (I', J); each
+// loads its own A panel and HALF of the shared B panel, multicast into both
+// CTAs' stages -- 16 KB of L2 reads per CTA and stage instead of 24 KB (the
+// single-CTA kernel runs at the L2->SM bandwidth, ~7.5 TB/s).  Stage s may
+// be refilled only when both CTAs' MMAs have read it, so each MMA commit
+// arrives on the empty barriers of both CTAs.  A tile with x < 0 is the
+// partner of an odd tile count: it loads and multiplies but does not drain.
+template <int CL>
 __global__ void __launch_bounds__(PRE_THREADS, 1)
 syrk_pre_kernel(const unsigned char* __restrict__ hi, const unsigned char* __restrict__ lo, int64_t ncp, int64_t nkb,
                 int64_t q, int64_t kchunk, const int2* __restrict__ tiles, double* __restrict__ G, int64_t ldg,
                 const unsigned* __restrict__ amax_bits) {
   using S = Split<true>;
   constexpr int STAGE = S::STAGE, A_BYTES = S::A_BYTES, B_BYTES = S::B_BYTES, LBO_A = S::LBO_A, LBO_B = S::LBO_B;
+  constexpr int BW = TN / CL;                                // B columns this CTA loads
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[PRE_NST], empty[PRE_NST], accf[2], acce[2];
   __shared__ uint32_t tmem_base_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int2 tile = tiles[blockIdx.x];
-  const int64_t i0 = (int64_t)tile.x * TM, j0 = (int64_t)tile.y * TN;
+  const bool drain = tile.x >= 0;
+  const int64_t i0 = (int64_t)(drain ? tile.x : -tile.x - 1) * TM, j0 = (int64_t)tile.y * TN;
+  uint32_t rank = 0;
+  if constexpr (CL > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int64_t nstages = nkb / 2;                          // 16 rows per stage
   const int64_t nchunks = (nstages * BK + kchunk - 1) / kchunk;
   const int64_t SPC = kchunk / BK;
@@ -433,7 +445,7 @@ syrk_pre_kernel(const unsigned char* __restrict__ hi, const unsigned char* __res
   if (tid == 0) {
     for (int s = 0; s < PRE_NST; ++s) {
       bar_init(&full[s], 1);
-      bar_init(&empty[s], 1);
+      bar_init(&empty[s], CL);
     }
     for (int a = 0; a < 2; ++a) {
       bar_init(&accf[a], 1);
@@ -448,13 +460,17 @@ syrk_pre_kernel(const unsigned char* __restrict__ hi, const unsigned char* __res
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if constexpr (CL > 1) {   // peers' barriers are initialised before anyone multicasts into them
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_s;
 
   if (warp == 5) {
-    // ===================== loader: 8 bulk copies per stage =====================
+    // ===================== loader =====================
     if (lane == 0) {
       const int64_t row_bytes = ncp * 16;                   // one 8-row block, all columns
+      const uint16_t mask = (uint16_t)((1u << CL) - 1u);
       for (int64_t it = 0; it < nstages; ++it) {
         const int s = (int)(it % PRE_NST);
         if (it >= PRE_NST) bar_wait(&empty[s], (unsigned)(((it / PRE_NST) - 1) & 1));
@@ -469,15 +485,22 @@ syrk_pre_kernel(const unsigned char* __restrict__ hi, const unsigned char* __res
           for (int part = 0; part < 2; ++part) {
             const unsigned char* base = srcs[part] + kb * row_bytes;
             const uint32_t da = st + part * A_BYTES + kc * LBO_A;
-            const uint32_t db = st + 2 * A_BYTES + part * B_BYTES + kc * LBO_B;
+            const uint32_t db = st + 2 * A_BYTES + part * B_BYTES + kc * LBO_B + rank * (BW * 16);
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(da),
                 "l"(base + i0 * 16), "r"((unsigned)(TM * 16)), "r"(bar)
                 : "memory");
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(db),
-                "l"(base + j0 * 16), "r"((unsigned)(TN * 16)), "r"(bar)
-                : "memory");
+            if constexpr (CL > 1)
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, "
+                  "[%3], %4;" ::"r"(db),
+                  "l"(base + (j0 + rank * BW) * 16), "r"((unsigned)(BW * 16)), "r"(bar), "h"(mask)
+                  : "memory");
+            else
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(db),
+                  "l"(base + j0 * 16), "r"((unsigned)(TN * 16)), "r"(bar)
+                  : "memory");
           }
         }
       }
@@ -502,7 +525,14 @@ syrk_pre_kernel(const unsigned char* __restrict__ hi, const unsigned char* __res
           mma_split<true>(d, dah, dbh, it > it0 ? 1u : 0u);
           mma_split<true>(d, dah, dbl, 1u);
           mma_split<true>(d, dal, dbh, 1u);
-          mma_commit(&empty[s]);
+          if constexpr (CL > 1)
+            asm volatile(
+                "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                    su32(&empty[s])),
+                "h"((uint16_t)((1u << CL) - 1u))
+                : "memory");
+          else
+            mma_commit(&empty[s]);
         }
         mma_commit(&accf[acc]);
       }
@@ -516,7 +546,7 @@ syrk_pre_kernel(const unsigned char* __restrict__ hi, const unsigned char* __res
       const int acc = (int)(c & 1);
       bar_wait(&accf[acc], (unsigned)((c >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      drain_chunk(tmem, warp, acc, i, j0, q, G, ldg, unscale);
+      if (drain) drain_chunk(tmem, warp, acc, i, j0, q, G, ldg, unscale);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) bar_arrive(&acce[acc]);
@@ -524,6 +554,9 @@ syrk_pre_kernel(const unsigned char* __restrict__ hi, const unsigned char* __res
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if constexpr (CL > 1) {   // no CTA leaves while its peer may still write or arrive into its shared memory
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
@@ -626,9 +659,23 @@ void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, vo
                     st>>>((const float*)A->data, A->m, A->ld, q, amax);
     GF_CHECK_LAUNCH();
     if (pre) {
+      // cluster pairs share a B panel: per column block bj the tiles bi are
+      // paired in order; an odd count gets a non-draining partner
+      const char* ce = getenv("GF_SYRK_CLUSTER");
+      const bool cl2 = !(ce && ce[0] == '1');
+      std::vector<int2> tl2;
+      for (int64_t bj = 0; bj < bj_n; ++bj) {
+        int cnt = 0;
+        for (int64_t bi = 2 * bj; bi < bi_n; ++bi, ++cnt) tl2.push_back(make_int2((int)bi, (int)bj));
+        if (cnt & 1) tl2.push_back(make_int2((int)(-(bi_n - 1) - 1), (int)bj));
+      }
+      DBuf d_tiles2(cl2 ? tl2.size() * sizeof(int2) : 0);
+      if (cl2)
+        GF_CUDA(cudaMemcpyAsync(d_tiles2.p, tl2.data(), tl2.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
       static bool pre_attr = false;
       if (!pre_attr) {
-        GF_CUDA(cudaFuncSetAttribute(syrk_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PRE_SMEM));
+        GF_CUDA(cudaFuncSetAttribute(syrk_pre_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, PRE_SMEM));
+        GF_CUDA(cudaFuncSetAttribute(syrk_pre_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, PRE_SMEM));
         pre_attr = true;
       }
       const char* vb = getenv("GF_VERBOSE_SETUP");
@@ -643,8 +690,25 @@ void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, vo
           (const float*)A->data, A->m, A->ld, q, ncp, nkb, amax, (uint4*)hi, (uint4*)lo);
       GF_CHECK_LAUNCH();
       if (verbose) GF_CUDA(cudaEventRecord(ev[1], st));
-      syrk_pre_kernel<<<(unsigned)tl.size(), PRE_THREADS, PRE_SMEM, st>>>(hi, lo, ncp, nkb, q, kchunk,
-                                                                        d_tiles.as<int2>(), G, ldg, amax);
+      if (cl2) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)tl2.size());
+        cfg.blockDim = dim3(PRE_THREADS);
+        cfg.dynamicSmemBytes = PRE_SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        GF_CUDA(cudaLaunchKernelEx(&cfg, syrk_pre_kernel<2>, (const unsigned char*)hi, (const unsigned char*)lo, ncp,
+                                   nkb, q, kchunk, (const int2*)d_tiles2.as<int2>(), G, ldg, (const unsigned*)amax));
+      } else {
+        syrk_pre_kernel<1><<<(unsigned)tl.size(), PRE_THREADS, PRE_SMEM, st>>>(hi, lo, ncp, nkb, q, kchunk,
+                                                                           d_tiles.as<int2>(), G, ldg, amax);
+      }
       GF_CHECK_LAUNCH();
       if (verbose) GF_CUDA(cudaEventRecord(ev[2], st));
       if (verbose) {
