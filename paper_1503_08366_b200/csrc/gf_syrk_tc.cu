@@ -606,16 +606,18 @@ size_t gram_scratch_bytes(const gf_matrix* A, bool tall) {
 // like their bit patterns); the padding columns are not read
 __global__ void absmax_kernel(const float* __restrict__ A, int64_t m, int64_t ld, int64_t n,
                               unsigned* __restrict__ out) {
-  const int64_t nv = (n + 3) / 4;
+  const int nv = (int)((n + 3) / 4);
   float mx = 0.0f;
-  for (int64_t i = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; i < m * nv; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / nv, v = i - r * nv;
-    const float4 a = reinterpret_cast<const float4*>(A + r * ld)[v];
-    const int64_t j = 4 * v;
-    mx = fmaxf(mx, fabsf(a.x));
-    if (j + 1 < n) mx = fmaxf(mx, fabsf(a.y));
-    if (j + 2 < n) mx = fmaxf(mx, fabsf(a.z));
-    if (j + 3 < n) mx = fmaxf(mx, fabsf(a.w));
+  for (int64_t r = blockIdx.x; r < m; r += gridDim.x) {
+    const float4* row = reinterpret_cast<const float4*>(A + r * ld);
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+      const float4 a = row[v];
+      const int j = 4 * v;
+      mx = fmaxf(mx, fabsf(a.x));
+      if (j + 1 < n) mx = fmaxf(mx, fabsf(a.y));
+      if (j + 2 < n) mx = fmaxf(mx, fabsf(a.z));
+      if (j + 3 < n) mx = fmaxf(mx, fabsf(a.w));
+    }
   }
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(mx));
@@ -654,9 +656,8 @@ void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, vo
   unsigned* amax = reinterpret_cast<unsigned*>(d_tiles.as<char>() + tl.size() * sizeof(int2) + 8);
   if (f16) {
     GF_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned), st));
-    const int64_t items = A->m * ceil_div(q, 4);
-    absmax_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), num_sms() * 8)), 256, 0,
-                    st>>>((const float*)A->data, A->m, A->ld, q, amax);
+    absmax_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(A->m, num_sms() * 8)), 256, 0, st>>>(
+        (const float*)A->data, A->m, A->ld, q, amax);
     GF_CHECK_LAUNCH();
     if (pre) {
       // cluster pairs share a B panel: per column block bj the tiles bi are
