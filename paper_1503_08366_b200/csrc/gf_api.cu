@@ -84,7 +84,7 @@ void allreduce_sum(gf_comm* c, double* buf, size_t count, cudaStream_t st) {
   if (r != ncclSuccess) throw_error(GF_E_NCCL, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
 }
 
-// Grow-only per-device scratch (plain cudaMalloc, kept for the process) for
+// Grow-only per-device scratch (from the retained pool, kept for the process) for
 // large setup temporaries; a ScratchLock holds the device's arena for the
 // duration of one projector build.
 struct ScratchArena {
@@ -104,10 +104,13 @@ struct ScratchLock {
   ScratchLock() : a(arena_for_current_device()), lk(a.mu) {}
   void* get(int i, size_t bytes) {   // slot i, grown to at least `bytes`
     if (a.bytes[i] < bytes) {
-      if (a.p[i]) GF_CUDA(cudaFree(a.p[i]));
+      // from the stream-ordered pool, whose reserve gf_init pre-maps: a plain
+      // cudaMalloc of the Gram's 4 GB pre-split copy cost ~0.3 s on first use
+      if (a.p[i]) GF_CUDA(cudaFreeAsync(a.p[i], 0));
       a.p[i] = nullptr;
       a.bytes[i] = 0;
-      GF_CUDA(cudaMalloc(&a.p[i], bytes));
+      GF_CUDA(cudaMallocAsync(&a.p[i], bytes, 0));
+      GF_CUDA(cudaStreamSynchronize(0));
       a.bytes[i] = bytes;
     }
     return a.p[i];
