@@ -256,13 +256,18 @@ def test_c1_headline_values():
     assert res.objective == pytest.approx(252.42917798604532, rel=1e-9)
 
 
-@pytest.mark.parametrize("split", ["f16", "tf32"])
+@pytest.mark.parametrize("split", ["pre", "pre1", "f16", "tf32"])
 @pytest.mark.parametrize("shape", [(513, 129), (3000, 700), (20000, 1300)])
 def test_gram_tensor_core_fp32(shape, split, monkeypatch):
     """The fp32 Gram runs on tcgen05 (scaled-fp16 or TF32 three-product split,
     fp64 drain every 1024 rows): it must agree with the fp64 Gram of the same
-    fp32 data to fp32-grade accuracy, including ragged tile edges."""
-    monkeypatch.setenv("GF_SYRK", split)
+    fp32 data to fp32-grade accuracy, including ragged tile edges.  pre: the
+    default pre-split copy in 2-CTA clusters (1300 columns: an odd tile count
+    per column block, so a non-draining partner CTA); pre1: single CTAs;
+    f16 / tf32: in-kernel converters."""
+    monkeypatch.setenv("GF_SYRK", "pre" if split == "pre1" else split)
+    if split == "pre1":
+        monkeypatch.setenv("GF_SYRK_CLUSTER", "1")
     m, n = shape
     A = np.random.default_rng(m + n).normal(size=(m, n)).astype(np.float32)
     G = gf.build_projector(A).gram
