@@ -257,7 +257,7 @@ def test_c1_headline_values():
 
 
 @pytest.mark.parametrize("split", ["pre", "pre1", "f16", "tf32"])
-@pytest.mark.parametrize("shape", [(513, 129), (3000, 700), (20000, 1300)])
+@pytest.mark.parametrize("shape", [(17, 17), (300, 257), (513, 129), (3000, 700), (20000, 1300)])
 def test_gram_tensor_core_fp32(shape, split, monkeypatch):
     """The fp32 Gram runs on tcgen05 (scaled-fp16 or TF32 three-product split,
     fp64 drain every 1024 rows): it must agree with the fp64 Gram of the same
@@ -278,6 +278,14 @@ def test_gram_tensor_core_fp32(shape, split, monkeypatch):
     # 1024 rows: measured ~5e-6 (tools/syrk_accuracy.py); plain TF32 gives ~4e-4
     assert err < 1.5e-5, err
     np.testing.assert_allclose(G, G.T, rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("split", ["pre", "f16"])
+def test_gram_f16_split_zero_matrix(split, monkeypatch):
+    """An all-zero matrix (max|A| = 0: scale 1) gives G = I exactly."""
+    monkeypatch.setenv("GF_SYRK", split)
+    G = gf.build_projector(np.zeros((1000, 130), np.float32)).gram
+    np.testing.assert_array_equal(G, np.eye(130))
 
 
 @pytest.mark.parametrize("scale", [1e-30, 1e-6, 1e6, 1e30])
