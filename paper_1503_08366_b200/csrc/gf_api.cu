@@ -214,7 +214,7 @@ static void check_terms(const gf_terms* t) {
 }
 
 static gf_projector* projector_build(gf_matrix* A, int mode, double tol, int64_t max_inner, gf_comm* comm,
-                                     cudaStream_t st) {
+                                     cudaStream_t st, const unsigned* amax_known = nullptr) {
   GF_REQUIRE(mode == 0 || mode == 1, GF_E_PARAMETER, "unknown projection mode");
   GF_REQUIRE(tol > 0.0, GF_E_PARAMETER, "projection tolerance must be positive");
   std::unique_ptr<gf_projector> P(new gf_projector());
@@ -257,7 +257,7 @@ static gf_projector* projector_build(gf_matrix* A, int mode, double tol, int64_t
     if (gsb - sl.a.bytes[3] + (1ull << 30) >= free_b) gsb = 0;
   }
   if (gsb > 0) gscratch = sl.get(3, gsb);
-  if (A->m > 0 && A->n > 0) gram_accumulate(A, P->tall, P->gram.as<double>(), P->ldg, st, gscratch, gsb);
+  if (A->m > 0 && A->n > 0) gram_accumulate(A, P->tall, P->gram.as<double>(), P->ldg, st, gscratch, gsb, amax_known);
   if (comm_active(comm)) allreduce_sum(comm, P->gram.as<double>(), (size_t)q * P->ldg, st);
   gram_finish(P->gram.as<double>(), q, P->ldg, st);
   pt.mark("gram");
@@ -661,8 +661,10 @@ int gf_setup_create(gf_matrix* A, int equil, const double* d_in, const double* e
       copy_in(S->d.as<double>(), ones.data(), A->m, st);
       copy_in(S->e.as<double>(), ones.data(), A->n, st);
     }
-    scale_matrix(A, S->d.as<double>(), S->e.as<double>(), st);
-    S->P = projector_build(A, mode, tol, max_inner, comm, st);
+    DBuf amax(sizeof(unsigned));   // max |A_hat| for the Gram's fp16 split, from the scaling pass
+    GF_CUDA(cudaMemsetAsync(amax.p, 0, sizeof(unsigned), st));
+    scale_matrix(A, S->d.as<double>(), S->e.as<double>(), st, amax.as<unsigned>());
+    S->P = projector_build(A, mode, tol, max_inner, comm, st, amax.as<unsigned>());
     S->A = A;  // ownership transferred on success only
     GF_CUDA(cudaStreamSynchronize(st));
     S->info.setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

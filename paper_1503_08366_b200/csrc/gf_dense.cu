@@ -256,13 +256,13 @@ __global__ void mirror_lower(double* G, int64_t q, int64_t ld) {
 static dim3 grid2(int64_t q) { return dim3((unsigned)ceil_div(q, 32), (unsigned)ceil_div(q, 8)); }
 
 void gram_accumulate(const gf_matrix* A, bool tall, double* G, int64_t ldg, cudaStream_t st, void* scratch,
-                     size_t scratch_bytes) {
+                     size_t scratch_bytes, const unsigned* amax_known) {
   const int64_t q = tall ? A->n : A->m;
   if (A->dtype == GF_F32) {
     const float* a = (const float*)A->data;
     const char* env = getenv("GF_GRAM_SIMT");
     if (tall && !(env && env[0] == '1')) {   // tensor cores: tcgen05 split (gf_syrk_tc.cu)
-      gram_tf32x3(A, G, ldg, st, scratch, scratch_bytes);
+      gram_tf32x3(A, G, ldg, st, scratch, scratch_bytes, amax_known);
       return;
     }
     if (tall) gemm<float, float, true, false>(q, q, A->m, 1.0, a, A->ld, a, A->ld, 0.0, G, ldg, true, st);

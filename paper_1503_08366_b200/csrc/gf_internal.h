@@ -70,9 +70,9 @@ struct DBuf {
 // (0 when the f16 pre-split path does not apply); `scratch` may be null.
 size_t gram_scratch_bytes(const gf_matrix* A, bool tall);
 void gram_accumulate(const gf_matrix* A, bool tall, double* G, int64_t ldg, cudaStream_t st,
-                     void* scratch = nullptr, size_t scratch_bytes = 0);
+                     void* scratch = nullptr, size_t scratch_bytes = 0, const unsigned* amax_known = nullptr);
 void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, void* scratch = nullptr,
-                 size_t scratch_bytes = 0);  // tcgen05, G += A'A
+                 size_t scratch_bytes = 0, const unsigned* amax_known = nullptr);  // tcgen05, G += A'A
 void gram_finish(double* G, int64_t q, int64_t ldg, cudaStream_t st);
 int cholesky(double* G, int64_t q, int64_t ld, int* d_info, cudaStream_t st);
 void trtri(double* L, int64_t q, int64_t ld, double* tmp, cudaStream_t st);
@@ -83,7 +83,8 @@ void store_matrix(const double* src, int64_t lds, int dtype, void* dst, int64_t 
 // --------------------------------------------------- matrices (gf_matrix) --
 void matrix_upload(gf_matrix* M, const void* src, int src_dtype, int64_t src_ld, cudaStream_t st);
 void matrix_to_f64(const gf_matrix* M, double* dst_dev, cudaStream_t st);  // dense m x n
-void scale_matrix(gf_matrix* M, const double* d, const double* e, cudaStream_t st);
+// amax (optional, zeroed by the caller): max |A_hat| over the real columns, as float bits
+void scale_matrix(gf_matrix* M, const double* d, const double* e, cudaStream_t st, unsigned* amax = nullptr);
 // y = A x (x: n) / y = A' x (x: m); fp64 device vectors; ws >= matvec_ws_bytes.
 void matvec(const gf_matrix* A, bool transpose, const double* x, double* y, cudaStream_t st);
 // y = (A o A) x / (A o A)' x (equilibration diagnostics, p = 2).

@@ -175,12 +175,17 @@ __device__ __forceinline__ T scale1(T a, double dr, double ej) {
 
 // One CTA per row (grid-stride), 16-byte vectors: A is read and written
 // once (2 m n s bytes); columns past n are the zero padding and stay zero.
+// With `amax` set, max |A_hat| over the real columns is accumulated as float
+// bits (non-negative floats order like their bits) for the Gram's fp16 split
+// scale, saving it a pass over A_hat.
 template <typename T>
 __global__ void __launch_bounds__(256) scale_kernel(T* __restrict__ A, int64_t rows, int64_t ld, int64_t n,
-                                                    const double* __restrict__ d, const double* __restrict__ e) {
+                                                    const double* __restrict__ d, const double* __restrict__ e,
+                                                    unsigned* __restrict__ amax) {
   using V = typename Vec16<T>::type;
   constexpr int VN = Vec16<T>::n;
   const int64_t nv = (n + VN - 1) / VN;
+  float mx = 0.0f;
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     const double dr = d[r];
     V* row = reinterpret_cast<V*>(A + r * ld);
@@ -192,20 +197,26 @@ __global__ void __launch_bounds__(256) scale_kernel(T* __restrict__ A, int64_t r
         if (j + 1 < n) a.y = scale1(a.y, dr, e[j + 1]);
         if (j + 2 < n) a.z = scale1(a.z, dr, e[j + 2]);
         if (j + 3 < n) a.w = scale1(a.w, dr, e[j + 3]);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf((float)a.x), fabsf((float)a.y)), fmaxf(fabsf((float)a.z), fabsf((float)a.w))));
       } else {
         a.x = scale1(a.x, dr, e[j]);
         if (j + 1 < n) a.y = scale1(a.y, dr, e[j + 1]);
+        mx = fmaxf(mx, fmaxf(fabsf((float)a.x), fabsf((float)a.y)));
       }
       row[v] = a;
     }
   }
+  if (amax != nullptr) {   // (padding lanes hold zeros: they do not raise the max)
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(amax, __float_as_uint(mx));
+  }
 }
 
-void scale_matrix(gf_matrix* M, const double* d, const double* e, cudaStream_t st) {
+void scale_matrix(gf_matrix* M, const double* d, const double* e, cudaStream_t st, unsigned* amax) {
   if (M->m == 0) return;
   const unsigned grid = (unsigned)std::min<int64_t>(M->m, (int64_t)num_sms() * 8);
-  if (M->dtype == GF_F32) scale_kernel<float><<<grid, 256, 0, st>>>((float*)M->data, M->m, M->ld, M->n, d, e);
-  else scale_kernel<double><<<grid, 256, 0, st>>>((double*)M->data, M->m, M->ld, M->n, d, e);
+  if (M->dtype == GF_F32) scale_kernel<float><<<grid, 256, 0, st>>>((float*)M->data, M->m, M->ld, M->n, d, e, amax);
+  else scale_kernel<double><<<grid, 256, 0, st>>>((double*)M->data, M->m, M->ld, M->n, d, e, amax);
   GF_CHECK_LAUNCH();
 }
 

@@ -625,7 +625,8 @@ __global__ void absmax_kernel(const float* __restrict__ A, int64_t m, int64_t ld
 
 // G (fp64, zeroed by the caller) += A'A for fp32 A (m x ld, columns >= n zero).
 // Default split: scaled fp16 hi/lo (kind::f16); GF_SYRK=tf32 selects 3xTF32.
-void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, void* scratch, size_t scratch_bytes) {
+void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, void* scratch, size_t scratch_bytes,
+                 const unsigned* amax_known) {
   using namespace syrk;
   const int64_t q = A->n;
   const int64_t bi_n = ceil_div(q, TM), bj_n = ceil_div(q, TN);
@@ -655,10 +656,14 @@ void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, vo
   const CUtensorMap tmA = panel_map(A, TM), tmB = panel_map(A, TN);
   unsigned* amax = reinterpret_cast<unsigned*>(d_tiles.as<char>() + tl.size() * sizeof(int2) + 8);
   if (f16) {
-    GF_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned), st));
-    absmax_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(A->m, num_sms() * 8)), 256, 0, st>>>(
-        (const float*)A->data, A->m, A->ld, q, amax);
-    GF_CHECK_LAUNCH();
+    if (amax_known != nullptr) {   // max |A_hat| from the scaling pass
+      GF_CUDA(cudaMemcpyAsync(amax, amax_known, sizeof(unsigned), cudaMemcpyDeviceToDevice, st));
+    } else {
+      GF_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned), st));
+      absmax_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(A->m, num_sms() * 8)), 256, 0, st>>>(
+          (const float*)A->data, A->m, A->ld, q, amax);
+      GF_CHECK_LAUNCH();
+    }
     if (pre) {
       // cluster pairs share a B panel: per column block bj the tiles bi are
       // paired in order; an odd count gets a non-draining partner
