@@ -410,9 +410,14 @@ __global__ void __launch_bounds__(256) split_f16_kernel(const float* __restrict_
   }
 }
 
-constexpr int PRE_NST = 8;                                  // 8 x 24 KB operand stages
+// 16-row slabs per stage: the per-stage round trip (copies land -> MMAs ->
+// commit -> slot refilled) costs about as much as a slab's MMAs, so stages
+// are 4 slabs (96 KB, 12 MMAs) deep and only two are needed: 1 slab per
+// stage 16.7 ms, 2 -> 15.0 ms, 4 -> 14.1 ms at 200000 x 5000
+constexpr int PRE_SUB = 4;
+constexpr int PRE_NST = 8 / PRE_SUB;                        // 192 KB of operand stages
 constexpr int PRE_THREADS = 6 * 32;                         // epilogue 0-3, MMA 4, loader 5
-constexpr int PRE_SMEM = PRE_NST * Split<true>::STAGE;
+constexpr int PRE_SMEM = PRE_NST * PRE_SUB * Split<true>::STAGE;
 
 // CL = 2: a cluster of two CTAs computes tiles (I, J) and (I', J); each
 // loads its own A panel and HALF of the shared B panel, multicast into both
@@ -438,9 +443,9 @@ syrk_pre_kernel(const unsigned char* __restrict__ hi, const unsigned char* __res
   const int64_t i0 = (int64_t)(drain ? tile.x : -tile.x - 1) * TM, j0 = (int64_t)tile.y * TN;
   uint32_t rank = 0;
   if constexpr (CL > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-  const int64_t nstages = nkb / 2;                          // 16 rows per stage
-  const int64_t nchunks = (nstages * BK + kchunk - 1) / kchunk;
-  const int64_t SPC = kchunk / BK;
+  const int64_t nstages = nkb / (2 * PRE_SUB);              // 16 PRE_SUB rows per stage
+  const int64_t nchunks = (nstages * BK * PRE_SUB + kchunk - 1) / kchunk;
+  const int64_t SPC = kchunk / (BK * PRE_SUB);
 
   if (tid == 0) {
     for (int s = 0; s < PRE_NST; ++s) {
@@ -474,12 +479,16 @@ syrk_pre_kernel(const unsigned char* __restrict__ hi, const unsigned char* __res
       for (int64_t it = 0; it < nstages; ++it) {
         const int s = (int)(it % PRE_NST);
         if (it >= PRE_NST) bar_wait(&empty[s], (unsigned)(((it / PRE_NST) - 1) & 1));
-        const uint32_t st = su32(smem + (size_t)s * STAGE), bar = su32(&full[s]);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)STAGE)
+        const uint32_t st0 = su32(smem + (size_t)s * PRE_SUB * STAGE), bar = su32(&full[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"((unsigned)(PRE_SUB * STAGE))
                      : "memory");
 #pragma unroll
+        for (int sub = 0; sub < PRE_SUB; ++sub)
+#pragma unroll
         for (int kc = 0; kc < 2; ++kc) {
-          const int64_t kb = 2 * it + kc;
+          const int64_t kb = 2 * (it * PRE_SUB + sub) + kc;
+          const uint32_t st = st0 + sub * STAGE;
           const unsigned char* srcs[2] = {hi, lo};
 #pragma unroll
           for (int part = 0; part < 2; ++part) {
@@ -518,13 +527,16 @@ syrk_pre_kernel(const unsigned char* __restrict__ hi, const unsigned char* __res
           const int s = (int)(it % PRE_NST);
           bar_wait(&full[s], (unsigned)((it / PRE_NST) & 1));
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t st = su32(smem + (size_t)s * STAGE);
-          const uint32_t a_hi = st, a_lo = st + A_BYTES, b_hi = st + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
-          const uint64_t dah = smem_desc(a_hi, LBO_A, 128), dal = smem_desc(a_lo, LBO_A, 128);
-          const uint64_t dbh = smem_desc(b_hi, LBO_B, 128), dbl = smem_desc(b_lo, LBO_B, 128);
-          mma_split<true>(d, dah, dbh, it > it0 ? 1u : 0u);
-          mma_split<true>(d, dah, dbl, 1u);
-          mma_split<true>(d, dal, dbh, 1u);
+#pragma unroll
+          for (int sub = 0; sub < PRE_SUB; ++sub) {
+            const uint32_t st = su32(smem + ((size_t)s * PRE_SUB + sub) * STAGE);
+            const uint32_t a_hi = st, a_lo = st + A_BYTES, b_hi = st + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
+            const uint64_t dah = smem_desc(a_hi, LBO_A, 128), dal = smem_desc(a_lo, LBO_A, 128);
+            const uint64_t dbh = smem_desc(b_hi, LBO_B, 128), dbl = smem_desc(b_lo, LBO_B, 128);
+            mma_split<true>(d, dah, dbh, (it > it0 || sub > 0) ? 1u : 0u);
+            mma_split<true>(d, dah, dbl, 1u);
+            mma_split<true>(d, dal, dbh, 1u);
+          }
           if constexpr (CL > 1)
             asm volatile(
                 "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -598,7 +610,7 @@ static CUtensorMap panel_map(const gf_matrix* A, int box_cols) {
 size_t gram_scratch_bytes(const gf_matrix* A, bool tall) {
   const char* sp = getenv("GF_SYRK");   // "tf32" / "f16": the in-kernel converters, no copy
   if (!tall || A->dtype != GF_F32 || (sp && (std::string(sp) == "tf32" || std::string(sp) == "f16"))) return 0;
-  const int64_t ncp = ceil_div(A->n, syrk::TN) * syrk::TN, nkb = ceil_div(A->m, syrk::BK) * 2;
+  const int64_t ncp = ceil_div(A->n, syrk::TN) * syrk::TN, nkb = ceil_div(A->m, syrk::BK * syrk::PRE_SUB) * 2 * syrk::PRE_SUB;
   return 2 * (size_t)nkb * ncp * 16;
 }
 
@@ -638,7 +650,7 @@ void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, vo
   GF_CUDA(cudaMemcpyAsync(d_tiles.p, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
   const char* sp = getenv("GF_SYRK");
   const bool f16 = !(sp && std::string(sp) == "tf32");
-  const int64_t ncp = ceil_div(q, TN) * TN, nkb = ceil_div(A->m, BK) * 2;
+  const int64_t ncp = ceil_div(q, TN) * TN, nkb = ceil_div(A->m, BK * PRE_SUB) * 2 * PRE_SUB;
   const size_t pre_bytes = (size_t)nkb * ncp * 16;          // each of hi, lo
   const bool pre = f16 && scratch != nullptr && scratch_bytes >= 2 * pre_bytes;
   static bool attr[2] = {false, false};
