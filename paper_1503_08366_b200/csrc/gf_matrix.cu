@@ -189,21 +189,34 @@ __global__ void __launch_bounds__(256) scale_kernel(T* __restrict__ A, int64_t r
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     const double dr = d[r];
     V* row = reinterpret_cast<V*>(A + r * ld);
-    for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
-      V a = row[v];
-      const int64_t j = v * VN;
-      if constexpr (VN == 4) {
-        a.x = scale1(a.x, dr, e[j]);
-        if (j + 1 < n) a.y = scale1(a.y, dr, e[j + 1]);
-        if (j + 2 < n) a.z = scale1(a.z, dr, e[j + 2]);
-        if (j + 3 < n) a.w = scale1(a.w, dr, e[j + 3]);
-        mx = fmaxf(mx, fmaxf(fmaxf(fabsf((float)a.x), fabsf((float)a.y)), fmaxf(fabsf((float)a.z), fabsf((float)a.w))));
-      } else {
-        a.x = scale1(a.x, dr, e[j]);
-        if (j + 1 < n) a.y = scale1(a.y, dr, e[j + 1]);
-        mx = fmaxf(mx, fmaxf(fabsf((float)a.x), fabsf((float)a.y)));
+    // four vectors per thread loaded before any is written back (each element
+    // is read and written by the same thread): four 16-byte loads in flight
+    for (int64_t v0 = threadIdx.x; v0 < nv; v0 += 4 * (int64_t)blockDim.x) {
+      V a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t v = v0 + u * (int64_t)blockDim.x;
+        if (v < nv) a[u] = row[v];
       }
-      row[v] = a;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t v = v0 + u * (int64_t)blockDim.x;
+        if (v >= nv) break;
+        const int64_t j = v * VN;
+        if constexpr (VN == 4) {
+          a[u].x = scale1(a[u].x, dr, e[j]);
+          if (j + 1 < n) a[u].y = scale1(a[u].y, dr, e[j + 1]);
+          if (j + 2 < n) a[u].z = scale1(a[u].z, dr, e[j + 2]);
+          if (j + 3 < n) a[u].w = scale1(a[u].w, dr, e[j + 3]);
+          mx = fmaxf(mx, fmaxf(fmaxf(fabsf((float)a[u].x), fabsf((float)a[u].y)),
+                               fmaxf(fabsf((float)a[u].z), fabsf((float)a[u].w))));
+        } else {
+          a[u].x = scale1(a[u].x, dr, e[j]);
+          if (j + 1 < n) a[u].y = scale1(a[u].y, dr, e[j + 1]);
+          mx = fmaxf(mx, fmaxf(fabsf((float)a[u].x), fabsf((float)a[u].y)));
+        }
+        row[v] = a[u];
+      }
     }
   }
   if (amax != nullptr) {   // (padding lanes hold zeros: they do not raise the max)
