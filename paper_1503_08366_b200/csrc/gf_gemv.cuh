@@ -129,7 +129,7 @@ constexpr int kColThreads = 256;
 
 // part layout: [slab][k][ld]; SQ: use A_rj^2 (equilibration) instead of A_rj.
 template <typename T, int NRHS, bool SQ>
-__global__ void __launch_bounds__(kColThreads)
+__global__ void __launch_bounds__(kColThreads, 4)   // plan_cols sizes the grid for 4 CTAs/SM
 colgemv_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const double* __restrict__ w0,
                const double* __restrict__ w1, int64_t rows_per_slab, double* __restrict__ part,
                const int* __restrict__ status) {
@@ -146,18 +146,24 @@ colgemv_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const double* 
   for (int i = 0; i < VN; ++i) { acc0[i] = 0.0; acc1[i] = 0.0; }
   if (cv < nvec) {
     const V* base = reinterpret_cast<const V*>(A) + cv;
-    int64_t r = r0;
-    for (; r + 3 < r1; r += 4) {
-      V a[4];
-      double u0[4], u1[4];
+    // U rows per step, every load issued before the first FMA (guarded loads
+    // like the scaling pass; unguarded ones were scheduled load-use-load);
+    // rows are accumulated in order, so the result does not depend on U
+    constexpr int U = 4;
+    for (int64_t r = r0; r < r1; r += U) {
+      V a[U];
+      double u0[U], u1[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        a[u] = ld_stream(base + (r + u) * nvec);
-        u0[u] = __ldg(w0 + r + u);
-        if (NRHS > 1) u1[u] = __ldg(w1 + r + u);
+      for (int u = 0; u < U; ++u) {
+        if (r + u < r1) {
+          a[u] = ld_stream(base + (r + u) * nvec);
+          u0[u] = __ldg(w0 + r + u);
+          if (NRHS > 1) u1[u] = __ldg(w1 + r + u);
+        }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < U; ++u) {
+        if (r + u >= r1) break;
 #pragma unroll
         for (int i = 0; i < VN; ++i) {
           double x = (double)vget(a[u], i);
@@ -165,17 +171,6 @@ colgemv_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const double* 
           acc0[i] = fma(x, u0[u], acc0[i]);
           if (NRHS > 1) acc1[i] = fma(x, u1[u], acc1[i]);
         }
-    }
-    for (; r < r1; ++r) {
-      const V a = ld_stream(base + r * nvec);
-      const double u0 = __ldg(w0 + r);
-      const double u1 = NRHS > 1 ? __ldg(w1 + r) : 0.0;
-#pragma unroll
-      for (int i = 0; i < VN; ++i) {
-        double x = (double)vget(a, i);
-        if (SQ) x = x * x;
-        acc0[i] = fma(x, u0, acc0[i]);
-        if (NRHS > 1) acc1[i] = fma(x, u1, acc1[i]);
       }
     }
     double* p0 = part + (slab * NRHS) * ld + cv * VN;
