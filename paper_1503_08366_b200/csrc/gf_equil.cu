@@ -33,12 +33,14 @@ sq_row_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, int64_t n, cons
     const V* ar = reinterpret_cast<const V*>(A + r * ld);
     double acc = 0.0;
     int64_t v = lane;
-    for (; v + 96 < nvec; v += 128) {   // four 16-byte loads in flight per lane
-      V a[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = ld_stream(ar + v + 32 * u);
+    for (; v < nvec; v += 128) {   // four guarded 16-byte loads issued together per lane
+      V a[4];                      // (unguarded, ptxas scheduled them load-use-load)
 #pragma unroll
       for (int u = 0; u < 4; ++u)
+        if (v + 32 * u < nvec) a[u] = ld_stream(ar + v + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (v + 32 * u >= nvec) break;
 #pragma unroll
         for (int i = 0; i < VN; ++i) {
           const int64_t j = (v + 32 * u) * VN + i;
@@ -46,16 +48,6 @@ sq_row_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, int64_t n, cons
             const double x = (double)vget(a[u], i);
             acc = fma(x * x, __ldg(w + j), acc);
           }
-        }
-    }
-    for (; v < nvec; v += 32) {
-      const V a = ld_stream(ar + v);
-#pragma unroll
-      for (int i = 0; i < VN; ++i) {
-        const int64_t j = v * VN + i;
-        if (j < n) {
-          const double x = (double)vget(a, i);
-          acc = fma(x * x, __ldg(w + j), acc);
         }
       }
     }
