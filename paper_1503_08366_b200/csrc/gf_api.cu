@@ -172,6 +172,12 @@ static int guarded(F&& fn) {
   }
 }
 
+template <typename F>
+static int guarded(void* stream, F&& fn) {
+  StreamScope scope((cudaStream_t)stream);
+  return guarded(std::forward<F>(fn));
+}
+
 static bool host_ptr(const void* p) {
   cudaPointerAttributes at{};
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -353,7 +359,7 @@ int gf_init(int device) {
 }
 
 int gf_prox_separable(const gf_terms* t, const double* rho, const double* v, double* out, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     check_terms(t);
     TermsView view{t->h, t->a, t->b, t->c, t->d, t->e};
     prox_separable(view, t->n, rho, v, out, (cudaStream_t)stream);
@@ -362,7 +368,7 @@ int gf_prox_separable(const gf_terms* t, const double* rho, const double* v, dou
 }
 
 int gf_prox_base(int64_t n, int kind, const double* rho, const double* v, double* out, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     GF_REQUIRE(kind >= 0 && kind <= 9, GF_E_PARAMETER, "unknown base function code");
     prox_base(kind, n, rho, v, out, (cudaStream_t)stream);
     GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
@@ -370,7 +376,7 @@ int gf_prox_base(int64_t n, int kind, const double* rho, const double* v, double
 }
 
 int gf_evaluate(const gf_terms* t, const double* v, double* result, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     check_terms(t);
     TermsView view{t->h, t->a, t->b, t->c, t->d, t->e};
     *result = evaluate(view, t->n, v, (cudaStream_t)stream);
@@ -378,7 +384,7 @@ int gf_evaluate(const gf_terms* t, const double* v, double* result, void* stream
 }
 
 int gf_eval_base(int64_t n, int kind, const double* x, double* out, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     GF_REQUIRE(kind >= 0 && kind <= 9, GF_E_PARAMETER, "unknown base function code");
     eval_base(kind, n, x, out, (cudaStream_t)stream);
     GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
@@ -388,7 +394,7 @@ int gf_eval_base(int64_t n, int kind, const double* x, double* out, void* stream
 int gf_normal_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
                    double loc, double scale, int dtype, void* out, int64_t ncol, int64_t rs, int64_t cs,
                    void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     GF_REQUIRE(dtype == GF_F32 || dtype == GF_F64, GF_E_PARAMETER, "dtype must be GF_F32 or GF_F64");
     GF_REQUIRE(count >= 0 && ncol >= 1, GF_E_DIMENSION, "count must be >= 0 and ncol >= 1");
     normal_fill(state_hi, state_lo, inc_hi, inc_lo, count, loc, scale, dtype, out, ncol, rs, cs,
@@ -398,7 +404,7 @@ int gf_normal_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64
 
 int gf_dense_matvec(int dtype, int64_t m, int64_t n, const void* A, int64_t lda, int transpose, const double* x,
                     double* y, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     GF_REQUIRE(dtype == GF_F32 || dtype == GF_F64, GF_E_PARAMETER, "dtype must be GF_F32 or GF_F64");
     const int64_t es = dtype == GF_F32 ? 4 : 8;
     GF_REQUIRE(m >= 0 && n >= 0 && lda >= n, GF_E_DIMENSION, "bad matrix shape / row stride");
@@ -416,7 +422,7 @@ int gf_dense_matvec(int dtype, int64_t m, int64_t n, const void* A, int64_t lda,
 }
 
 int gf_rows_affine(int64_t m, int64_t n, double* A, int64_t lda, const double* s, const double* t, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     rows_affine(m, n, A, lda, s, t, (cudaStream_t)stream);
     GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   });
@@ -424,7 +430,7 @@ int gf_rows_affine(int64_t m, int64_t n, double* A, int64_t lda, const double* s
 
 int gf_convert_matrix(int64_t m, int64_t n, const double* src, int64_t lds, int dtype, void* dst, int64_t ldd,
                       void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     GF_REQUIRE(dtype == GF_F32 || dtype == GF_F64, GF_E_PARAMETER, "dtype must be GF_F32 or GF_F64");
     store_matrix(src, lds, dtype, dst, ldd, m, n, (cudaStream_t)stream);
     GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
@@ -432,7 +438,7 @@ int gf_convert_matrix(int64_t m, int64_t n, const double* src, int64_t lds, int 
 }
 
 int gf_conj_base(int64_t n, int kind, const double* w, double* out, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     GF_REQUIRE(kind >= 0 && kind <= 9, GF_E_PARAMETER, "unknown base function code");
     conj_base(kind, n, w, out, (cudaStream_t)stream);
     GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
@@ -440,7 +446,7 @@ int gf_conj_base(int64_t n, int kind, const double* w, double* out, void* stream
 }
 
 int gf_conjugate(const gf_terms* t, const double* w, double* result, int* supported, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     check_terms(t);
     TermsView view{t->h, t->a, t->b, t->c, t->d, t->e};
     bool ok = true;
@@ -451,7 +457,7 @@ int gf_conjugate(const gf_terms* t, const double* w, double* result, int* suppor
 
 int gf_matrix_create(int dtype, int64_t m, int64_t n, const void* src, int src_dtype, int64_t src_ld, void* stream,
                      gf_matrix** out) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     GF_REQUIRE(dtype == GF_F32 || dtype == GF_F64, GF_E_PARAMETER, "dtype must be GF_F32 or GF_F64");
     GF_REQUIRE(src_dtype == GF_F32 || src_dtype == GF_F64, GF_E_PARAMETER, "bad source dtype");
     GF_REQUIRE(m >= 0 && n >= 1, GF_E_DIMENSION, "matrix must have at least one column");
@@ -491,7 +497,7 @@ int gf_matrix_shape(const gf_matrix* A, int64_t* m, int64_t* n, int64_t* ld, int
 }
 
 int gf_matrix_download(const gf_matrix* A, double* dst, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     cudaStream_t st = (cudaStream_t)stream;
     if (A->m == 0) return;
     DBuf tmp((size_t)A->m * A->n * sizeof(double));
@@ -502,7 +508,7 @@ int gf_matrix_download(const gf_matrix* A, double* dst, void* stream) {
 }
 
 int gf_matvec(const gf_matrix* A, int transpose, const double* x, double* y, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t nx = transpose ? A->m : A->n, ny = transpose ? A->n : A->m;
     DevVec xv(x, nx, st);
@@ -517,7 +523,7 @@ int gf_matvec(const gf_matrix* A, int transpose, const double* x, double* y, voi
 }
 
 int gf_sq_matvec(const gf_matrix* A, int transpose, const double* x, double* y, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t nx = transpose ? A->m : A->n, ny = transpose ? A->n : A->m;
     DevVec xv(x, nx, st);
@@ -535,7 +541,7 @@ int gf_sq_matvec(const gf_matrix* A, int transpose, const double* x, double* y, 
 int gf_equilibrate_observed(gf_matrix* A, double gamma, double eps, int64_t max_iter, gf_comm* comm, double* d, double* e,
                    int64_t* sweeps, int* converged, double* gamma_used, gf_sweep_fn on_sweep, void* user,
                             void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     cudaStream_t st = (cudaStream_t)stream;
     DBuf dd(std::max<int64_t>(A->m, 1) * sizeof(double)), ee(A->n * sizeof(double));
     const EquilResult r = equilibrate(A, gamma, eps, max_iter, comm, dd.as<double>(), ee.as<double>(), st,
@@ -556,7 +562,7 @@ int gf_equilibrate(gf_matrix* A, double gamma, double eps, int64_t max_iter, gf_
 
 
 int gf_rescale_even(gf_matrix* A, double* d, double* e, gf_comm* comm, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     cudaStream_t st = (cudaStream_t)stream;
     DBuf dd(std::max<int64_t>(A->m, 1) * sizeof(double)), ee(A->n * sizeof(double));
     copy_in(dd.as<double>(), d, A->m, st);
@@ -569,7 +575,7 @@ int gf_rescale_even(gf_matrix* A, double* d, double* e, gf_comm* comm, void* str
 }
 
 int gf_scale_matrix(gf_matrix* A, const double* d, const double* e, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     cudaStream_t st = (cudaStream_t)stream;
     DevVec dv(d, A->m, st), ev(e, A->n, st);
     scale_matrix(A, dv.p, ev.p, st);
@@ -579,7 +585,7 @@ int gf_scale_matrix(gf_matrix* A, const double* d, const double* e, void* stream
 
 int gf_projector_create(gf_matrix* A, int mode, double tol, int64_t max_inner, gf_comm* comm, void* stream,
                         gf_projector** out) {
-  return guarded([&] { *out = projector_build(A, mode, tol, max_inner, comm, (cudaStream_t)stream); });
+  return guarded(stream, [&] { *out = projector_build(A, mode, tol, max_inner, comm, (cudaStream_t)stream); });
 }
 
 int gf_projector_destroy(gf_projector* P) {
@@ -587,7 +593,7 @@ int gf_projector_destroy(gf_projector* P) {
 }
 
 int gf_projector_gram(const gf_projector* P, double* out, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     GF_REQUIRE(P->mode == 0, GF_E_PARAMETER, "indirect projectors have no Gram matrix");
     cudaStream_t st = (cudaStream_t)stream;
     GF_CUDA(cudaMemcpy2DAsync(out, P->q * sizeof(double), P->gram.p, P->ldg * sizeof(double), P->q * sizeof(double),
@@ -597,7 +603,7 @@ int gf_projector_gram(const gf_projector* P, double* out, void* stream) {
 }
 
 int gf_project(gf_projector* P, const double* c, const double* d, double* x, double* y, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     GF_REQUIRE(P->mode == 0, GF_E_PARAMETER, "project requires a direct-mode cache; use project_indirect");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t m = P->A->m, n = P->A->n;
@@ -613,7 +619,7 @@ int gf_project(gf_projector* P, const double* c, const double* d, double* x, dou
 int gf_project_indirect(gf_projector* P, const double* c, const double* d, const double* x_warm,
                         const double* y_warm, double tol, double* x, double* y, int64_t* iterations, int* converged,
                         void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     GF_REQUIRE(tol > 0.0, GF_E_PARAMETER, "projection tolerance must be positive");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t m = P->A->m, n = P->A->n;
@@ -633,7 +639,7 @@ int gf_project_indirect(gf_projector* P, const double* c, const double* d, const
 
 int gf_setup_create(gf_matrix* A, int equil, const double* d_in, const double* e_in, int mode, double tol,
                     int64_t max_inner, gf_comm* comm, void* stream, gf_setup** out) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     cudaStream_t st = (cudaStream_t)stream;
     const auto t0 = std::chrono::steady_clock::now();
     std::unique_ptr<gf_setup> S(new gf_setup());
@@ -686,7 +692,7 @@ int gf_setup_get_info(const gf_setup* S, gf_setup_info* info) {
 }
 
 int gf_setup_scaling(const gf_setup* S, double* d, double* e, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     cudaStream_t st = (cudaStream_t)stream;
     if (d) copy_out(d, S->d.as<double>(), S->A->m, st);
     if (e) copy_out(e, S->e.as<double>(), S->A->n, st);
@@ -704,7 +710,7 @@ int gf_setup_matrix(gf_setup* S, gf_matrix** A) {
 
 int gf_solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, const gf_settings* settings,
                      const double* x0, const double* nu0, void* stream, gf_solver** out) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     check_terms(f);
     check_terms(g);
     GF_REQUIRE(settings->max_iter >= 1, GF_E_PARAMETER, "max_iter must be at least 1");
@@ -713,20 +719,20 @@ int gf_solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, const gf
 }
 
 int gf_solver_run(gf_solver* s, int64_t steps, gf_solver_state* st, void* stream) {
-  return guarded([&] { solver_run(s, steps, st, (cudaStream_t)stream); });
+  return guarded(stream, [&] { solver_run(s, steps, st, (cudaStream_t)stream); });
 }
 
 int gf_solver_history(gf_solver* s, int64_t count, double* out, void* stream) {
-  return guarded([&] { solver_history(s, count, out, (cudaStream_t)stream); });
+  return guarded(stream, [&] { solver_history(s, count, out, (cudaStream_t)stream); });
 }
 
 int gf_solver_snapshot(gf_solver* s, double* x_hat, double* y_hat, double* xt, double* yt, double* x_half_hat,
                        double* y_half_hat, void* stream) {
-  return guarded([&] { solver_snapshot(s, x_hat, y_hat, xt, yt, x_half_hat, y_half_hat, (cudaStream_t)stream); });
+  return guarded(stream, [&] { solver_snapshot(s, x_hat, y_hat, xt, yt, x_half_hat, y_half_hat, (cudaStream_t)stream); });
 }
 
 int gf_solver_result(gf_solver* s, double* x, double* y, double* mu, double* nu, gf_solver_state* st, void* stream) {
-  return guarded([&] { solver_result(s, x, y, mu, nu, st, (cudaStream_t)stream); });
+  return guarded(stream, [&] { solver_result(s, x, y, mu, nu, st, (cudaStream_t)stream); });
 }
 
 int gf_solver_destroy(gf_solver* s) {
@@ -736,7 +742,7 @@ int gf_solver_destroy(gf_solver* s) {
 int gf_solve(gf_setup* S, const gf_terms* f, const gf_terms* g, const gf_settings* settings, const double* x0,
              const double* nu0, double* x, double* y, double* mu, double* nu, gf_solver_state* st,
              double* history, void* stream) {
-  return guarded([&] {
+  return guarded(stream, [&] {
     check_terms(f);
     check_terms(g);
     GF_REQUIRE(settings->max_iter >= 1, GF_E_PARAMETER, "max_iter must be at least 1");

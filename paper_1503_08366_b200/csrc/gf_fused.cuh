@@ -557,4 +557,377 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
   }
 }
 
+
+// ============================================================================
+// Two-CTA cluster variant for wide rows (>= 40 KB: fp64 rows of 5000, fp32
+// rows of 10000).  With whole rows only five fit in shared memory (one row
+// per group: the serial epilogue then bounds the pass) and the compute warps
+// would need 160 KB of register-resident column state.  Here the two CTAs of
+// a cluster (two SMs) share one contiguous row range and split every row by
+// columns: CTA r streams only its half of each row (TMA bulk copies of
+// 20 KB), owns half of the column vectors (half the register state: the
+// 8-warp x 5-vector shape of the fp32 n = 5000 kernel) and writes its
+// half of the column slab.  Per group of TR rows the two CTAs exchange their
+// K = 2 TR partial row dots through distributed shared memory; both then
+// hold the full dots (summed as CTA 0's partial + CTA 1's: identical in
+// both), and row j of the group is finished by CTA (j & 1) only -- its
+// epilogue (prox, duals, stores, reductions) runs once, and its column-pass
+// weights are written into both CTAs' w_s before the arrivals on both wf
+// barriers (count 2: the local and the peer epilogue warp).
+//
+// Hand-offs added to the single-CTA pipeline (buffer b = group mod NE):
+//   xbuf[b]  peer's K partial dots, written remotely; xf[b] (count 1) is the
+//            peer's remote arrive.  A partial for use u is sent only after
+//            we[b] of use u-1 completed locally, so the peer can write this
+//            CTA's w_s[b] only once the local compute warps consumed it;
+//            xbuf[b] is free again by then too (the peer's next partial
+//            needs this CTA's wf arrival of use u, made after reading it).
+// Remote writes are st.shared::cluster by lane 0 followed by its
+// mbarrier.arrive.release.cluster; waiters that read remote data use
+// acquire.cluster.  A cluster barrier after the mbarrier init and one before
+// exit keep every remote access inside both CTAs' lifetimes.
+// ============================================================================
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cta address -> shared::cluster address of the same variable in CTA `rank`
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, double v) { st_cluster_f64(addr, v); }
+__device__ __forceinline__ void st_cluster(uint32_t addr, float v) { st_cluster_f32(addr, v); }
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster_u32(uint32_t bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(bar),
+      "r"(parity), "r"(kSuspendNs)
+      : "memory");
+}
+
+struct FusedPlan2 {
+  int cw = 0, ne = 0, nv = 0, nslot = 0, tr = 0;
+  int grid = 0;        // CTAs (2 per cluster)
+  int64_t hvec = 0;    // 16-byte vectors of a row in CTA 0's half (CTA 1: nvec - hvec)
+  size_t smem = 0;
+  bool ok = false;
+};
+
+// max_clusters: co-resident 2-CTA clusters at this shared-memory size
+// (cudaOccupancyMaxActiveClusters): the kernel is persistent, every cluster
+// must be resident in one wave.
+inline FusedPlan2 plan_fused_cl2(int64_t m, int64_t ld, int esize, int sms, size_t smem_max, int max_clusters) {
+  FusedPlan2 p;
+  const int vn = 16 / esize;
+  const int64_t nvec = ld / vn;
+  p.hvec = (nvec + 1) / 2;
+  p.cw = 20;
+  for (int cw : {8, 12, 16, 20})
+    if (ceil_div(p.hvec, cw * 32) <= (cw <= 12 ? 5 : 4)) { p.cw = cw; break; }
+  p.nv = (int)ceil_div(p.hvec, p.cw * 32);
+  p.ne = fused_epi(p.cw);
+  const size_t slot_bytes = (size_t)p.hvec * 16;
+  const size_t budget = smem_max > 8192 ? smem_max - 8192 : 0;
+  p.nslot = (int)std::min<size_t>(kMaxSlots, budget / slot_bytes);
+  const int want_pf = std::max<int>(2, (int)ceil_div(48 * 1024, (int64_t)slot_bytes));
+  p.tr = 0;
+  for (int tr : {4, 2, 1})
+    if (3 * tr + want_pf <= p.nslot || (tr == 1 && 3 + 1 <= p.nslot)) { p.tr = tr; break; }
+  const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms / 2, (int64_t)max_clusters, m}));
+  p.grid = (int)(2 * ncl);
+  p.smem = (size_t)p.nslot * slot_bytes;
+  p.ok = max_clusters >= 1 && p.hvec >= 1 && nvec - p.hvec >= 1 && p.nv >= 1 && p.nv <= 6 && p.tr >= 1 && m > 0;
+  return p;
+}
+
+template <typename T, int NV, int TR, int CW, class Epi>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fused_threads(CW), 1)
+fused_rowcol_cl2_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* __restrict__ x0,
+                        const T* __restrict__ x1, Epi epi, int nslot, int64_t hvec, double* __restrict__ rpart,
+                        double* __restrict__ cpart) {
+  using V = typename Vec16<T>::type;
+  constexpr int VN = Vec16<T>::n;
+  constexpr int NR = Epi::NR;
+  constexpr int K = 2 * TR;
+  constexpr int LGK = K == 2 ? 1 : (K == 4 ? 2 : 3);
+  constexpr int kFusedWarps = CW;
+  constexpr int kFusedThreads = CW * kWarp;
+  constexpr int NE = fused_epi(CW);
+  constexpr int kEpiWarp = CW;
+  constexpr int kProdWarp = CW + NE;
+  static_assert(CW <= 32, "one epilogue lane per compute warp");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[kMaxSlots], sfree[kMaxSlots];
+  __shared__ __align__(8) uint64_t redf[NE], rede[NE], wf[NE], we[NE], xf[NE];
+  __shared__ T red_s[NE][kFusedWarps][K];
+  __shared__ __align__(8) T w_s[NE][TR][2];
+  __shared__ __align__(8) double xbuf[NE][K];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = cluster_ctarank(), peer = rank ^ 1u;
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int64_t nvec_all = ld / VN;
+  const int64_t v0 = rank ? hvec : 0;                      // first 16-byte vector of this CTA's half
+  const int64_t nvec = rank ? nvec_all - hvec : hvec;      // vectors of this CTA's half
+  const unsigned sb = (unsigned)(hvec * 16);               // slot stride
+  const unsigned cb = (unsigned)(nvec * 16);               // bytes copied per row
+  const int64_t r0 = rows * cid / ncl;
+  const int64_t r1 = rows * (cid + 1) / ncl;
+  const int nr = (int)(r1 - r0);
+  const int ng = (nr + TR - 1) / TR;
+
+  if (tid == 0) {
+    for (int s = 0; s < nslot; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&sfree[s], kFusedWarps);
+    }
+    for (int b = 0; b < NE; ++b) {
+      mbar_init(&redf[b], kFusedWarps);
+      mbar_init(&rede[b], 1);
+      mbar_init(&wf[b], 2);
+      mbar_init(&we[b], kFusedWarps);
+      mbar_init(&xf[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  cluster_sync_all();   // the peer's barriers exist before any remote arrive
+
+  if (warp == kProdWarp) {
+    // ===================== producer warp =====================
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const int pre = min(nslot, nr);
+      for (int j = 0; j < pre; ++j) {
+        mbar_arrive_expect_tx(&full[j], cb);
+        bulk_g2s(smem_raw + j * sb, A + (r0 + j) * ld + v0 * VN, cb, &full[j], pol);
+      }
+      pdl_wait();
+      pdl_trigger();
+      if (!epi.active()) {
+        for (int j = 0; j < pre; ++j) mbar_wait(&full[j], 0u);
+      } else {
+        int slot = pre == nslot ? 0 : pre;
+        for (int j = pre; j < nr; ++j) {
+          if (j >= nslot) mbar_wait(&sfree[slot], (unsigned)(((j / nslot) - 1) & 1));
+          mbar_arrive_expect_tx(&full[slot], cb);
+          bulk_g2s(smem_raw + slot * sb, A + (r0 + j) * ld + v0 * VN, cb, &full[slot], pol);
+          if (++slot == nslot) slot = 0;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kEpiWarp && warp < kEpiWarp + NE) {
+    // ===================== epilogue warps =====================
+    pdl_wait();
+    if (epi.active()) {
+      const int par = warp - kEpiWarp;
+      const int b = par;
+      epi.begin();
+      double ered[NR > 0 ? NR : 1];
+#pragma unroll
+      for (int k = 0; k < (NR > 0 ? NR : 1); ++k) ered[k] = 0.0;
+      unsigned eflags = 0;
+      const uint32_t xb_peer = mapa_u32(smem_u32(&xbuf[b][0]), peer);
+      const uint32_t xf_peer = mapa_u32(smem_u32(&xf[b]), peer);
+      const uint32_t wf_peer = mapa_u32(smem_u32(&wf[b]), peer);
+      const uint32_t ws_peer = mapa_u32(smem_u32(&w_s[b][0][0]), peer);
+      const uint32_t xf_loc = smem_u32(&xf[b]);
+      typename Epi::RowIn in{};
+      if (lane < TR && par * TR + lane < nr) in = epi.load_in(r0 + par * TR + lane);
+      for (int ge = par; ge < ng; ge += NE) {
+        const unsigned use = (unsigned)(ge / NE);
+        mbar_wait(&redf[b], use & 1u);
+        constexpr int RW = CW <= 16 ? 16 : 32;
+        double v[K];
+#pragma unroll
+        for (int q = 0; q < K; ++q) v[q] = lane < kFusedWarps ? (double)red_s[b][lane][q] : 0.0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(&rede[b], 0);
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+#pragma unroll
+          for (int o = RW / 2; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o, RW);
+        if (use >= 1) mbar_wait(&we[b], (use - 1) & 1u);    // local w_s[b] consumed by C(ge - NE)
+        // this CTA's partials -> the peer
+        if (lane == 0) {
+#pragma unroll
+          for (int q = 0; q < K; ++q) st_cluster_f64(xb_peer + 8u * q, v[q]);
+          mbar_arrive_remote(xf_peer);
+        }
+        mbar_wait_cluster_u32(xf_loc, use & 1u);           // the peer's partials
+        const int g = min(TR, nr - ge * TR);
+        double dots[2] = {0.0, 0.0};
+#pragma unroll
+        for (int rr = 0; rr < TR; ++rr)
+          if (rr == lane) {
+            const double p0 = xbuf[b][2 * rr], p1 = xbuf[b][2 * rr + 1];
+            dots[0] = rank == 0 ? v[2 * rr] + p0 : p0 + v[2 * rr];
+            dots[1] = rank == 0 ? v[2 * rr + 1] + p1 : p1 + v[2 * rr + 1];
+          }
+        const bool mine = lane < g && (((ge * TR + lane) & 1) == (int)rank);
+        typename Epi::Mid md{};
+        double w0 = 0.0, w1 = 0.0;
+        if (mine) md = epi.mid(in, dots, w0, w1);
+        // lane 0 writes the weights of this CTA's rows into both CTAs' w_s
+        // and arrives on both wf[b]
+#pragma unroll
+        for (int rr = 0; rr < TR; ++rr) {
+          const double a0 = __shfl_sync(0xffffffffu, w0, rr);
+          const double a1 = __shfl_sync(0xffffffffu, w1, rr);
+          if (lane == 0 && rr < g && (((ge * TR + rr) & 1) == (int)rank)) {
+            w_s[b][rr][0] = (T)a0;
+            w_s[b][rr][1] = (T)a1;
+            st_cluster(ws_peer + (unsigned)((rr * 2) * sizeof(T)), (T)a0);
+            st_cluster(ws_peer + (unsigned)((rr * 2 + 1) * sizeof(T)), (T)a1);
+          }
+        }
+        if (lane == 0) {
+          mbar_arrive_remote(wf_peer);
+          mbar_arrive_expect_tx(&wf[b], 0);
+        }
+        if (mine) epi.tail(r0 + (int64_t)ge * TR + lane, in, dots, md, ered, eflags);
+        const int jn = (ge + NE) * TR + lane;
+        if (lane < TR && jn < nr) in = epi.load_in(r0 + jn);
+      }
+#pragma unroll
+      for (int k = 0; k < NR; ++k) ered[k] = warp_sum(ered[k]);
+      eflags = warp_or(eflags);
+      if (lane == 0) {
+        double* out = rpart + (NE * (int64_t)blockIdx.x + par) * (NR + 1);
+        for (int k = 0; k < NR; ++k) out[k] = ered[k];
+        out[NR] = (double)eflags;
+      }
+    } else if (lane == 0) {   // inactive: empty records keep the Z step's sums defined
+      double* out = rpart + (NE * (int64_t)blockIdx.x + (warp - kEpiWarp)) * (NR + 1);
+      for (int k = 0; k <= NR; ++k) out[k] = 0.0;
+    }
+    __syncwarp();
+  } else {
+    // ===================== compute warps =====================
+    pdl_wait();
+    if (epi.active()) {
+      V xa[NV], xb[NV], ca[NV], cb2[NV];
+      uint32_t voff[NV];
+      {
+        const V* xv0 = reinterpret_cast<const V*>(x0) + v0;
+        const V* xv1 = reinterpret_cast<const V*>(x1) + v0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int c = tid + v * kFusedThreads;
+          const bool ok = c < (int)nvec;
+          voff[v] = (uint32_t)(ok ? c : (int)nvec - 1) * 16u;
+          xa[v] = ok ? xv0[c] : V{};
+          xb[v] = ok ? xv1[c] : V{};
+          ca[v] = V{};
+          cb2[v] = V{};
+        }
+      }
+      const uint32_t ring0 = smem_u32(smem_raw);
+      const uint32_t full0 = smem_u32(full);
+      const uint32_t sfree0 = smem_u32(sfree);
+      const uint32_t redf0 = smem_u32(redf), rede0 = smem_u32(rede), wf0 = smem_u32(wf), we0 = smem_u32(we);
+      const bool red_writer = (lane & ((32 >> LGK) - 1)) == 0;
+      T* const red_dst = &red_s[0][warp][lane >> (5 - LGK)];
+      int slotR = 0, slotC = 0;
+      unsigned phaseR = 0;
+      int jR = 0, jC = 0;
+      int bR = 0, bC = 0;
+      unsigned useR = 0, useC = 0;
+      for (int t = 0; t < ng + 2; ++t) {
+        if (t < ng) {   // ---- R(t) ----
+          T s[K];
+#pragma unroll
+          for (int rr = 0; rr < TR; ++rr) {
+            s[2 * rr] = 0;
+            s[2 * rr + 1] = 0;
+            if (jR < nr) {
+              mbar_wait_u32(full0 + 8u * slotR, phaseR);
+              const uint32_t row = ring0 + (uint32_t)slotR * sb;
+              typename DotAcc<T>::type p0[NV], p1[NV];
+#pragma unroll
+              for (int v = 0; v < NV; ++v) {
+                const V a = lds128(row + voff[v], (V*)nullptr);
+                p0[v] = dot_acc(a, xa[v]);
+                p1[v] = dot_acc(a, xb[v]);
+              }
+#pragma unroll
+              for (int v = 1; v < NV; ++v) { p0[0] = dot_add(p0[0], p0[v]); p1[0] = dot_add(p1[0], p1[v]); }
+              s[2 * rr] = dot_fin(p0[0]);
+              s[2 * rr + 1] = dot_fin(p1[0]);
+              ++jR;
+              if (++slotR == nslot) { slotR = 0; phaseR ^= 1u; }
+            }
+          }
+          const T tot = warp_multi_sum<K>(s, lane);
+          if (useR >= 1) mbar_wait_u32(rede0 + 8u * bR, (useR - 1) & 1u);
+          if (red_writer) red_dst[bR * (kFusedWarps * K)] = tot;
+          __syncwarp();
+          if (lane == 0) mbar_arrive_u32(redf0 + 8u * bR);
+          if (++bR == NE) { bR = 0; ++useR; }
+        }
+        if (t >= 2) {   // ---- C(t-2) ----
+          mbar_wait_cluster_u32(wf0 + 8u * bC, useC & 1u);   // weights partly written by the peer
+          T w0[TR], w1[TR];
+#pragma unroll
+          for (int rr = 0; rr < TR; ++rr) { w0[rr] = w_s[bC][rr][0]; w1[rr] = w_s[bC][rr][1]; }
+          __syncwarp();
+          if (lane == 0) mbar_arrive_u32(we0 + 8u * bC);
+          if (++bC == NE) { bC = 0; ++useC; }
+#pragma unroll
+          for (int rr = 0; rr < TR; ++rr) {
+            if (jC < nr) {
+              const uint32_t row = ring0 + (uint32_t)slotC * sb;
+#pragma unroll
+              for (int v = 0; v < NV; ++v) {
+                const V a = lds128(row + voff[v], (V*)nullptr);
+                vaxpy(ca[v], a, w0[rr]);
+                vaxpy(cb2[v], a, w1[rr]);
+              }
+              __syncwarp();
+              if (lane == 0) mbar_arrive_u32(sfree0 + 8u * slotC);
+              ++jC;
+              if (++slotC == nslot) slotC = 0;
+            }
+          }
+        }
+      }
+      // this CTA's columns of the cluster's slab
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int64_t c = tid + (int64_t)v * kFusedThreads;
+        if (c < nvec) {
+          double* p0 = cpart + (cid * 2) * ld + (v0 + c) * VN;
+          double* p1 = cpart + (cid * 2 + 1) * ld + (v0 + c) * VN;
+#pragma unroll
+          for (int i = 0; i < VN; ++i) {
+            p0[i] = (double)vget(ca[v], i);
+            p1[i] = (double)vget(cb2[v], i);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();   // no CTA leaves while its peer may still access its shared memory
+}
+
 }  // namespace gf

@@ -36,11 +36,29 @@ inline bool comm_active(const gf_comm* c) { return c != nullptr && c->comm != nu
 
 namespace gf {
 
+// Stream of the API call in progress on this thread (set by the C entry
+// points that take a stream): DBuf scratch buffers are allocated and freed
+// in that stream's order, so a buffer released while kernels that use it are
+// still queued (e.g. an early CGLS exit) cannot be handed out again before
+// they ran -- also when the caller works on a non-blocking stream.
+inline cudaStream_t& tls_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  return s;
+}
+struct StreamScope {
+  cudaStream_t prev;
+  explicit StreamScope(cudaStream_t s) : prev(tls_stream()) { tls_stream() = s; }
+  ~StreamScope() { tls_stream() = prev; }
+};
+
 // Device buffer with RAII free, from the device's stream-ordered memory pool
-// (cudaMallocAsync on the legacy stream; gf_init raises the pool's release
-// threshold so freed blocks are reused instead of returned to the driver).
-// Plain cudaMalloc/cudaFree cost milliseconds and cudaFree synchronizes the
-// device, which showed up as ~0.3 s per solve in the end-to-end path.
+// (cudaMallocAsync on the current call's stream; gf_init raises the pool's
+// release threshold so freed blocks are reused instead of returned to the
+// driver).  Plain cudaMalloc/cudaFree cost milliseconds and cudaFree
+// synchronizes the device, which showed up as ~0.3 s per solve in the
+// end-to-end path.  Buffers owned by long-lived handles are freed by the
+// destroy calls (no stream: the legacy stream), after the API's result calls
+// have synchronized the stream they were used on.
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -50,14 +68,14 @@ struct DBuf {
   DBuf& operator=(const DBuf&) = delete;
   DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
   DBuf& operator=(DBuf&& o) noexcept { std::swap(p, o.p); std::swap(bytes, o.bytes); return *this; }
-  ~DBuf() { if (p) cudaFreeAsync(p, 0); }
+  ~DBuf() { if (p) cudaFreeAsync(p, tls_stream()); }
   void alloc(size_t b) {
-    if (p) cudaFreeAsync(p, 0);
+    if (p) cudaFreeAsync(p, tls_stream());
     p = nullptr;
     bytes = b;
     if (b) {
       const auto t0 = std::chrono::steady_clock::now();
-      GF_CUDA(cudaMallocAsync(&p, b, 0));
+      GF_CUDA(cudaMallocAsync(&p, b, tls_stream()));
       const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
       if (ms > 2.0 && getenv("GF_VERBOSE_SETUP")) fprintf(stderr, "[gf] slow alloc %zu bytes: %.1f ms\n", b, ms);
     }

@@ -293,18 +293,78 @@ struct WEpi {
   }
 };
 
+// Indirect wide step: the CGLS tolerance schedule needs the drift of
+// iteration k, sqrt(||x^_1/2 - x^||^2 + ||y^_1/2 - y^||^2) (solver.py:401-405),
+// before the controller runs: from the R(k) records and the x records of
+// X(k-1) / x-init.  out = [drift, status].
+__global__ void wide_drift_kernel(const Ctl* __restrict__ ctl, const double* __restrict__ rpart, int64_t nr,
+                                  const double* __restrict__ xpart, int64_t nx, double* __restrict__ out) {
+  __shared__ double sh[8];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < nr; i += blockDim.x) s += rpart[i * (kRedY + 1) + 3];
+  for (int64_t i = threadIdx.x; i < nx; i += blockDim.x) s += xpart[i * (kRedX + 1) + 2];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    out[0] = sqrt(t);
+    out[1] = (double)ctl->status;
+  }
+}
+
+// After the wide CGLS (w = z in place): y+ = c_y + w (projection.py:161) and
+// its finiteness flags, one word per CTA in the WEpi record layout.
+__global__ void __launch_bounds__(256) wide_cgls_finish_kernel(const double* __restrict__ cy,
+                                                               const double* __restrict__ w, double* __restrict__ ypl,
+                                                               int64_t m, double* __restrict__ spart) {
+  unsigned flags = 0;
+  for (int64_t i = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const double yp = A_(cy[i], w[i]);
+    ypl[i] = yp;
+    if (!isfinite(yp)) flags |= kBadYPlus;
+  }
+  flags = warp_or(flags);
+  __shared__ unsigned sf[8];
+  if ((threadIdx.x & 31) == 0) sf[threadIdx.x >> 5] = flags;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned f = 0;
+    for (int i = 0; i < 8; ++i) f |= sf[i];
+    spart[blockIdx.x] = (double)f;
+  }
+}
+
+__global__ void neg_diff_kernel(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out,
+                                double* __restrict__ neg_b, int64_t n) {
+  // out = a - b, neg_b = -b
+  for (int64_t i = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    out[i] = S_(a[i], b[i]);
+    neg_b[i] = -b[i];
+  }
+}
+
 // x side after the controller from an x+ given as a vector: wide schedule
 // x+ = c_x - A_hat' w (projection.py:126, sub = 1), or the CGLS solution of
 // the indirect mode (projection.py:148-150, sub = 0); then the dual step and
 // prox_g of iteration k+1.
+// xk_prev / xt_prev (wide only, may be null) keep x^ and x~ of the iteration
+// just recorded, which this kernel overwrites with those of the next one: a
+// trace snapshot of iteration k reads them (solver.py:362-367).
 template <typename T>
 __global__ void __launch_bounds__(256) x_wide_kernel(XEpi<T> epi, const double* __restrict__ aw,
-                                                     double* __restrict__ part, int sub) {
+                                                     double* __restrict__ part, int sub, double* __restrict__ xk_prev,
+                                                     double* __restrict__ xt_prev) {
   if (!epi.active()) return;
   double red[kRedX] = {};
   unsigned flags = 0;
   const double ratio = epi.ctl->ratio;
   for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < epi.n; j += (int64_t)gridDim.x * blockDim.x) {
+    if (xk_prev) {
+      xk_prev[j] = epi.xk[j];
+      xt_prev[j] = epi.xt[j];
+    }
     const double cxj = epi.cx[j];
     const double xp = sub ? S_(cxj, aw[j]) : aw[j];
     if (!sub && !isfinite(xp)) flags |= kBadXPlus;
@@ -894,6 +954,7 @@ struct gf_solver {
   bool indirect = false;   // CGLS projection (projection.py:130-162)
   double ptol = -1.0;      // fixed CGLS tolerance, <= 0: schedule
   DBuf ypl, wv, spart;   // wide: y+ of the last projection, w, Ginv-pass flags
+  DBuf xkp, xtp;         // wide: x^, x~ of the last recorded iteration (trace snapshots)
   DBuf xplus;            // indirect: CGLS iterate / x+
   Params prm{};
   TermsDev f, g;
@@ -904,6 +965,7 @@ struct gf_solver {
   int64_t grid_r = 1, grid_s = 1, grid_z = 1, grid_zt = 1;
   ColPlan cplan;
   FusedPlan fplan;
+  FusedPlan2 fplan2;  // two-CTA cluster variant (rows of 40 KB and more)
   RingPlan rplan;     // S step on the TMA row ring (tall, direct)
   int warm_x = 0;
   int64_t next_step = 0;  // step k = [S(k-1)], R(k), C(k), Z(k)
@@ -913,6 +975,7 @@ struct gf_solver {
   cudaEvent_t ev_done[2] = {nullptr, nullptr};   // controller snapshots of in-flight chunks
   double elapsed_ms = 0.0;
   int64_t launches = 0;  // kernels launched by solver_run
+  int64_t inner_host = 0;  // H2D source of the last CGLS count (wide indirect)
   // optional per-kernel timing (gf_solver_profile): events around each launch
   bool profile = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -1049,6 +1112,57 @@ static void fused_dispatch(gf_solver* s, cudaStream_t st, bool attr_only) {
   }
 }
 
+// Two-CTA cluster variant.  attr_only: set the shared-memory limit and
+// return the number of co-resident clusters of this instance.
+template <typename T, int NV, int TR, int CW>
+static int fused2_go(gf_solver* s, cudaStream_t st, bool attr_only) {
+  const FusedPlan2& p = s->fplan2;
+  auto kern = fused_rowcol_cl2_kernel<T, NV, TR, CW, YEpi<T>>;
+  if (attr_only) {
+    GF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * (num_sms() / 2)));
+    cfg.blockDim = dim3(fused_threads(CW));
+    cfg.dynamicSmemBytes = p.smem;
+    int ncl = 0;
+    GF_CUDA(cudaOccupancyMaxActiveClusters(&ncl, (void*)kern, &cfg));
+    return ncl;
+  }
+  launch_k(use_pdl(s), kern, dim3(p.grid), dim3(fused_threads(CW)), p.smem, st, (const T*)s->S->A->data, s->m,
+           s->ld, (const T*)s->xk_T.as<T>(), (const T*)s->xh_T.as<T>(), make_yepi<T>(s), p.nslot, p.hvec,
+           s->rpart.as<double>(), s->cpart.as<double>());
+  GF_CHECK_LAUNCH();
+  return 0;
+}
+
+template <typename T, int NV, int CW>
+static int fused2_tr(gf_solver* s, cudaStream_t st, bool attr_only) {
+  return s->fplan2.tr >= 2 ? fused2_go<T, NV, 2, CW>(s, st, attr_only) : fused2_go<T, NV, 1, CW>(s, st, attr_only);
+}
+
+template <typename T>
+static int fused2_dispatch(gf_solver* s, cudaStream_t st, bool attr_only) {
+  const int nv = s->fplan2.nv;
+  switch (s->fplan2.cw) {
+    case 8:
+      switch (nv) {
+        case 1: case 2: case 3: return fused2_tr<T, 3, 8>(s, st, attr_only);
+        case 4: return fused2_tr<T, 4, 8>(s, st, attr_only);
+        default: return fused2_tr<T, 5, 8>(s, st, attr_only);
+      }
+    case 12:
+      return nv == 4 ? fused2_tr<T, 4, 12>(s, st, attr_only) : fused2_tr<T, 5, 12>(s, st, attr_only);
+    case 16:
+      return fused2_tr<T, 4, 16>(s, st, attr_only);
+    default:
+      switch (nv) {
+        case 4: return fused2_tr<T, 4, 20>(s, st, attr_only);
+        case 5: return fused2_tr<T, 5, 20>(s, st, attr_only);
+        default: return fused2_tr<T, 6, 20>(s, st, attr_only);
+      }
+  }
+}
+
 template <typename T>
 static XEpi<T> make_xepi(gf_solver* s);
 
@@ -1140,7 +1254,7 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
                                      s->xplus.as<double>(), ptol, P->max_inner, &ok, st);
     GF_CUDA(cudaMemcpyAsync(&ctl->inner, &inner, sizeof(int64_t), cudaMemcpyHostToDevice, st));
     x_wide_kernel<T><<<(unsigned)s->grid_s, 256, 0, st>>>(make_xepi<T>(s), s->xplus.as<double>(),
-                                                            s->xpart.as<double>(), 0);
+                                                            s->xpart.as<double>(), 0, nullptr, nullptr);
     GF_CHECK_LAUNCH();
     GF_CUDA(cudaStreamSynchronize(st));   // `inner` lives on this stack frame
     s->launches += 1;
@@ -1163,6 +1277,13 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
       s->mark(7, st, false);
       slabs = s->fplan.grid;
       nrpart = s->fplan.ne * s->fplan.grid;   // one record per epilogue warp
+      s->launches += 1;
+    } else if (s->fplan2.ok) {   // the same single pass, rows split over 2-CTA clusters
+      s->mark(7, st, true);
+      fused2_dispatch<T>(s, st, false);
+      s->mark(7, st, false);
+      slabs = s->fplan2.grid / 2;              // one slab per cluster
+      nrpart = s->fplan2.ne * s->fplan2.grid;
       s->launches += 1;
     } else {             // two passes: row pass (+ y side), then column pass
       s->mark(1, st, true);
@@ -1234,12 +1355,44 @@ static void launch_step_wide(gf_solver* s, int64_t k, cudaStream_t st) {
       (const T*)A->data, s->m, s->ld, s->xk_T.as<T>(), s->xh_T.as<T>(), ye, s->rpart.as<double>());
   GF_CHECK_LAUNCH();
   s->mark(1, st, false);
-  WEpi we{ctl, s->cy.as<double>(), s->wv.as<double>(), s->ypl.as<double>()};
-  s->mark(0, st, true);
-  rowgemv_kernel<T, 1, WEpi><<<(unsigned)s->grid_s, kRowThreads, 0, st>>>(
-      P->ginv.as<T>(), s->q, s->ldq, s->rhs_T.as<T>(), s->rhs_T.as<T>(), we, s->spart.as<double>());
-  GF_CHECK_LAUNCH();
-  s->mark(0, st, false);
+  if (s->indirect) {
+    // Indirect projection of iteration k (projection.py:152-161, solver.py:
+    // 397-411): CGLS on (I + A A') w = A c_x - c_y warm-started at
+    // z0 = y^ - c_y, tolerance from the drift schedule unless fixed; then
+    // y+ = c_y + w, and x+ = c_x - A' w comes from the column pass.  Like the
+    // direct wide step it runs before the controller (a solve that stops at
+    // k discards it).  The reference's tolerance schedule stalls wide
+    // problems at MaxIterations: reproduced, not fixed.
+    double hs[2] = {0.0, 0.0};
+    wide_drift_kernel<<<1, 256, 0, st>>>(ctl, s->rpart.as<double>(), s->grid_r, s->xpart.as<double>(), s->grid_s,
+                                         s->xplus.as<double>());
+    GF_CHECK_LAUNCH();
+    GF_CUDA(cudaMemcpyAsync(hs, s->xplus.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    GF_CUDA(cudaStreamSynchronize(st));
+    if ((int)hs[1] == GF_STATUS_RUNNING) {
+      const double ptol = s->ptol > 0.0 ? s->ptol : std::min(1e-2, std::max(1e-10, 0.1 * hs[0]));
+      DBuf negcy(std::max<int64_t>(s->m, 1) * sizeof(double));
+      neg_diff_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(s->m, 256), 1024)), 256, 0, st>>>(
+          s->yk.as<double>(), s->cy.as<double>(), s->wv.as<double>(), negcy.as<double>(), s->m);
+      GF_CHECK_LAUNCH();
+      bool ok = false;
+      const int64_t inner = cgls_solve(A, false, s->S->comm, s->cx.as<double>(), negcy.as<double>(),
+                                       s->wv.as<double>(), ptol, P->max_inner, &ok, st);
+      s->inner_host = inner;
+      GF_CUDA(cudaMemcpyAsync(&ctl->inner, &s->inner_host, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+      wide_cgls_finish_kernel<<<(unsigned)s->grid_s, 256, 0, st>>>(s->cy.as<double>(), s->wv.as<double>(),
+                                                                  s->ypl.as<double>(), s->m, s->spart.as<double>());
+      GF_CHECK_LAUNCH();
+      GF_CUDA(cudaStreamSynchronize(st));   // negcy and the H2D source
+    }
+  } else {
+    WEpi we{ctl, s->cy.as<double>(), s->wv.as<double>(), s->ypl.as<double>()};
+    s->mark(0, st, true);
+    rowgemv_kernel<T, 1, WEpi><<<(unsigned)s->grid_s, kRowThreads, 0, st>>>(
+        P->ginv.as<T>(), s->q, s->ldq, s->rhs_T.as<T>(), s->rhs_T.as<T>(), we, s->spart.as<double>());
+    GF_CHECK_LAUNCH();
+    s->mark(0, st, false);
+  }
   s->mark(2, st, true);
   colgemv_kernel<T, 2, false><<<dim3((unsigned)s->cplan.col_blocks, (unsigned)s->cplan.slabs), kColThreads, 0, st>>>(
       (const T*)A->data, s->m, s->ld, s->wv.as<double>(), s->nuh2.as<double>() + (k & 1) * s->m,
@@ -1264,7 +1417,7 @@ static void launch_step_wide(gf_solver* s, int64_t k, cudaStream_t st) {
   s->mark(5, st, false);
   s->mark(0, st, true);
   x_wide_kernel<T><<<(unsigned)s->grid_s, 256, 0, st>>>(make_xepi<T>(s), s->red.as<double>(), s->xpart.as<double>(),
-                                                          1);
+                                                          1, s->xkp.as<double>(), s->xtp.as<double>());
   GF_CHECK_LAUNCH();
   s->mark(0, st, false);
   s->launches += 7;
@@ -1330,8 +1483,6 @@ static void fill_state(gf_solver* s, gf_solver_state* st) {
 gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, const gf_settings* st_in,
                          const double* x0, const double* nu0, cudaStream_t st) {
   GF_REQUIRE(S->P != nullptr, GF_E_PARAMETER, "setup has no projector");
-  GF_REQUIRE(S->P->mode == 0 || S->P->tall, GF_E_UNSUPPORTED,
-             "the indirect (CGLS) projection inside solve is available for tall problems (m >= n)");
   GF_REQUIRE(S->P->tall || !comm_active(S->comm), GF_E_UNSUPPORTED,
              "wide (m < n) problems are solved on one GPU (row partitions need m >= n)");
   std::unique_ptr<gf_solver> s(new gf_solver());
@@ -1350,8 +1501,23 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
   s->g.load(g, st);
   // gap stopping needs closed-form conjugates of every term; otherwise the
   // reference's gap is None and never stops (problem.py:79-84)
-  if (st_in->gap_stop)
-    s->prm.gap = (conj_supported(s->f.view, s->m, st) && conj_supported(s->g.view, s->n, st)) ? 1 : 0;
+  if (st_in->gap_stop) {
+    bool ok = conj_supported(s->f.view, s->m, st) && conj_supported(s->g.view, s->n, st);
+    if (comm_active(S->comm)) {
+      // f is row-partitioned: every rank must take the same decision, or
+      // ranks that test a partial gap stop while the others wait in the next
+      // all-reduce
+      DBuf flag(sizeof(double));
+      const double bad = ok ? 0.0 : 1.0;
+      GF_CUDA(cudaMemcpyAsync(flag.p, &bad, sizeof(double), cudaMemcpyHostToDevice, st));
+      allreduce_sum(S->comm, flag.as<double>(), 1, st);
+      double tot = 0.0;
+      GF_CUDA(cudaMemcpyAsync(&tot, flag.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+      GF_CUDA(cudaStreamSynchronize(st));
+      ok = tot == 0.0;
+    }
+    s->prm.gap = ok ? 1 : 0;
+  }
   const int sms = num_sms();
   const int64_t n = s->n, m1 = std::max<int64_t>(s->m, 1), es = A->esize();
   s->grid_r = row_grid(m1, sms);
@@ -1387,14 +1553,35 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
     // measured C2 logistic 100000 x 10000 fp32 1.52 vs 1.85 ms, SVM
     // 200000 x 5000 fp64 2.54 vs 2.85 ms per iteration.
     const char* force = getenv("GF_FORCE_FUSED");   // dev override for measurements
+    const bool one_row = s->fplan.tr == 1 || !s->fplan.ok;
     if (s->fplan.ok && s->fplan.tr == 1 && !(force && force[0] == '1')) s->fplan.ok = false;
     if (s->fplan.ok) {
       if (s->dtype == GF_F32) fused_prepare<float>(s.get());
       else fused_prepare<double>(s.get());
     }
+    // Rows of 40 KB and more: split each row over the two CTAs of a cluster
+    // (gf_fused.cuh, fused_rowcol_cl2_kernel) -- half the bytes per slot,
+    // two rows per group, half the column state per CTA.  GF_FUSED_CL2=0
+    // disables it, =1 forces it for any tall shape (measurements).
+    const char* cl2env = getenv("GF_FUSED_CL2");
+    const bool cl2_off = cl2env && cl2env[0] == '0', cl2_force = cl2env && cl2env[0] == '1';
+    if (s->tall && !cl2_off && (cl2_force || (one_row && !s->fplan.ok)) &&
+        !(env && env[0] == '1')) {
+      s->fplan2 = plan_fused_cl2(s->m, s->ld, (int)es, sms, (size_t)optin, sms / 2);
+      if (s->fplan2.ok && (s->fplan2.tr >= 2 || cl2_force)) {
+        const int ncl = s->dtype == GF_F32 ? fused2_dispatch<float>(s.get(), nullptr, true)
+                                           : fused2_dispatch<double>(s.get(), nullptr, true);
+        s->fplan2 = plan_fused_cl2(s->m, s->ld, (int)es, sms, (size_t)optin, ncl);
+        if (s->fplan2.ok) s->fplan.ok = false;
+      } else {
+        s->fplan2.ok = false;
+      }
+    }
   }
-  const int64_t nslab = std::max<int64_t>(s->cplan.slabs, s->fplan.ok ? s->fplan.grid : 1);
-  vec(s->rpart, std::max<int64_t>(s->grid_r, s->fplan.ok ? kFusedEpiMax * s->fplan.grid : 1) * (kRedY + 1));
+  const int64_t nslab = std::max<int64_t>({s->cplan.slabs, s->fplan.ok ? s->fplan.grid : 1,
+                                           s->fplan2.ok ? s->fplan2.grid / 2 : 1});
+  vec(s->rpart, std::max<int64_t>({s->grid_r, s->fplan.ok ? kFusedEpiMax * s->fplan.grid : 1,
+                                   s->fplan2.ok ? kFusedEpiMax * s->fplan2.grid : 1}) * (kRedY + 1));
   vec(s->xpart, s->grid_s * (kRedX + 1));
   vec(s->zpart, std::max(s->grid_z, s->grid_zt));
   vec(s->red, 2 * s->ld + 2 * kScal + kRedX + 1);   // + CTA 0's record sums (Z step)
@@ -1402,8 +1589,10 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
     vec(s->ypl, m1);
     vec(s->wv, m1);
     vec(s->spart, s->grid_s);
+    vec(s->xkp, n);
+    vec(s->xtp, n);
   }
-  if (s->indirect) vec(s->xplus, n);
+  if (s->indirect) vec(s->xplus, std::max<int64_t>(n, 2));
   s->cpart.alloc((size_t)nslab * 2 * s->ld * sizeof(double));
   const int64_t hrows = std::max<int64_t>(s->prm.max_iter, 1) + 1;
   vec(s->hist, hrows * 8);
@@ -1498,9 +1687,13 @@ void solver_snapshot(gf_solver* s, double* x_hat, double* y_hat, double* xt, dou
   snapshot_kernel<<<64, 256, 0, st>>>(s->ctl.as<Ctl>(), s->n, s->m, s->xh2.as<double>(), s->yh2.as<double>(),
                                       s->S->e.as<double>(), s->S->d.as<double>(), bx.as<double>(), by.as<double>());
   GF_CHECK_LAUNCH();
-  copy_out(x_hat, s->xk.as<double>(), s->n, st);
+  // wide: a step that did not end the solve ran X(k), which already holds
+  // x^ and x~ of iteration k + 1; iteration k's are in xkp / xtp
+  read_ctl(s, st);
+  const bool advanced = !s->tall && s->host.status == GF_STATUS_RUNNING && s->next_step > 0;
+  copy_out(x_hat, (advanced ? s->xkp : s->xk).as<double>(), s->n, st);
   copy_out(y_hat, s->yk.as<double>(), s->m, st);
-  copy_out(xt, s->xt.as<double>(), s->n, st);
+  copy_out(xt, (advanced ? s->xtp : s->xt).as<double>(), s->n, st);
   copy_out(yt, s->yt.as<double>(), s->m, st);
   copy_out(xhh, bx.as<double>(), s->n, st);
   copy_out(yhh, by.as<double>(), s->m, st);

@@ -48,7 +48,9 @@ class Equilibration:
 
 
 def _matrix_dtype(A):
-    return _native.GF_F32 if str(getattr(A, "dtype", "")).endswith("float32") else _native.GF_F64
+    # fp64 like the reference (equilibration.py:150 works on float64 A),
+    # whatever the input's storage type
+    return _native.GF_F64
 
 
 def _as_matrix(A):

@@ -100,8 +100,10 @@ def build_projector(A, mode: str = "direct", tol: float = 1e-8,
 
 
 def _dtype_for(A, precision):
+    # the reference coerces every input to float64 (problem.py:35); fp32
+    # arithmetic is opt-in only
     if precision is None:
-        return _native.GF_F32 if str(getattr(A, "dtype", "")).endswith("float32") else _native.GF_F64
+        return _native.GF_F64
     if precision in ("fp32", "float32"):
         return _native.GF_F32
     if precision in ("fp64", "float64"):

@@ -10,9 +10,10 @@ iteration at a time and reads the recorded iteration back, so the observable
 per-iteration values are the same.
 
 Extension (not in the reference): ``SolverSettings.precision`` selects the
-arithmetic type of the matrix passes -- "fp64", "fp32", or None to follow
-the dtype of A (float32 input -> fp32).  Term math, norms and the stopping
-rule are fp64 in both.
+arithmetic type of the matrix passes -- "fp64" (also what None means: the
+reference computes in float64 whatever the input, problem.py:35) or "fp32"
+(opt-in: A_hat and G^-1 stored and streamed in fp32).  Term math, norms and
+the stopping rule are fp64 in both.
 """
 
 from __future__ import annotations
@@ -187,6 +188,17 @@ class _MatrixView:
         return out
 
 
+def _global_rows(m_local: int) -> int:
+    """Sum of the ranks' row counts over the default torch.distributed group
+    (the group the communicator was built from)."""
+    import torch
+    import torch.distributed as dist
+    dev = _native.device() if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([m_local], dtype=torch.int64, device=dev)
+    dist.all_reduce(t)
+    return int(t.item())
+
+
 def prepare(problem: GraphFormProblem, settings: SolverSettings = None,
             scaling: Optional[Equilibration] = None, comm=None) -> Setup:
     """Equilibrate (unless disabled or supplied), scale A in place on the
@@ -200,7 +212,11 @@ def prepare(problem: GraphFormProblem, settings: SolverSettings = None,
     dt = _dtype_for(A, settings.precision)
     M = _native.Matrix(A, dt)
     tol = settings.projection_tol if settings.projection_tol is not None else 1e-8
-    max_inner = settings.max_inner if settings.max_inner is not None else max(100, 2 * min(m, n))
+    if settings.max_inner is not None:
+        max_inner = settings.max_inner
+    else:   # projection.py:146 on the GLOBAL row count (every rank the same CGLS cap)
+        mg = m if comm is None else _global_rows(m)
+        max_inner = max(100, 2 * min(mg, n))
     d_in = e_in = None
     if scaling is not None:
         if scaling.d.shape != (m,) or scaling.e.shape != (n,):
@@ -315,12 +331,16 @@ def solve(problem: GraphFormProblem, settings: SolverSettings = None, *,
         run.run(0)
     else:
         seen = -1
+        first = len(trace) if trace is not None else 0   # snapshots of THIS solve start here
+        indirect = settings.projection == "indirect"
+        wide = problem.m < problem.n
         while True:
             st = run.run(1)
             # a step begins with the (indirect) projection of the previous
             # iteration: its CGLS count belongs to the previous snapshot
-            # (solver.py:410-411)
-            if trace and settings.projection == "indirect" and st.k > seen:
+            # (solver.py:410-411) -- also when that step records nothing new
+            # (the projection of the last iteration, or a degenerate one)
+            if trace is not None and len(trace) > first and indirect and not wide:
                 trace[-1].inner_iterations = int(st.inner_iterations)
             if st.k > seen:
                 k = int(st.k)
@@ -337,6 +357,10 @@ def solve(problem: GraphFormProblem, settings: SolverSettings = None, *,
                                                    x_half_hat=xhh, y_half_hat=yhh, r_pri=float(r_pri),
                                                    r_dual=float(r_dual), eps_pri=float(eps_pri),
                                                    eps_dual=float(eps_dual), inner_iterations=0))
+                    # wide: the step that records iteration k also ran its
+                    # projection, unless iteration k stopped the solve
+                    if indirect and wide and st.status != 1:
+                        trace[-1].inner_iterations = int(st.inner_iterations)
             if st.status != 0:
                 break
     x, y, mu, nu, st = run.result()

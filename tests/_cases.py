@@ -42,7 +42,9 @@ def build_problem(fx, as_float32=False):
     m, n, seed = int(m), int(n), int(seed)
     r32 = kind.endswith("32")
     base = kind[:-2] if r32 else kind
-    if base in ("tall_lasso", "tall_ridge"):
+    if base.startswith("degen_"):   # explicit small matrix stored in the fixture
+        A = np.asarray(fx["A"], np.float64)
+    elif base in ("tall_lasso", "tall_ridge"):
         build = instances.tall_lasso if base == "tall_lasso" else instances.tall_ridge
         problem, _ = build(m, n, seed, dtype=np.float32 if r32 else np.float64)
         A = np.asarray(problem.A, np.float64)
@@ -68,3 +70,27 @@ def warm_of(fx):
     if "x0" in fx:
         return dict(x0=fx["x0"], nu0=fx["nu0"])
     return {}
+
+
+def same_scalar(a, ref, rtol):
+    """a == ref within rtol * max(1, |ref|); NaN matches NaN and an infinity
+    the same infinity (degenerate solves report non-finite objectives)."""
+    a, ref = float(a), float(ref)
+    if np.isnan(ref) or np.isinf(ref):
+        return (np.isnan(a) and np.isnan(ref)) or a == ref
+    return abs(a - ref) <= rtol * max(1.0, abs(ref))
+
+
+def close_vectors(a, b, rtol, atol):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    if a.shape != b.shape:
+        return False
+    with np.errstate(over="ignore", invalid="ignore"):
+        nb = np.linalg.norm(b)
+        if np.isfinite(nb) and np.all(np.isfinite(a)):
+            return bool(np.linalg.norm(a - b) <= rtol * nb + atol * np.sqrt(max(b.size, 1)))
+        fa, fb = np.isfinite(a), np.isfinite(b)
+        if not np.array_equal(fa, fb) or not np.array_equal(a[~fb], b[~fb], equal_nan=True):
+            return False
+        d = np.abs(a[fb] - b[fb])
+        return bool(np.all(d <= rtol * np.abs(b[fb]) + atol))

@@ -234,11 +234,39 @@ SOLVE_CASES = [
      {"gap_stop": True, "abs_tol": 1e-3, "rel_tol": 1e-2}, {}),
     ("lasso_tall_1000x200_gap", ("tall_lasso", 1000, 200, 0), {"gap_stop": True}, {}),
     ("nnls_600x150_gap", ("nnls", 600, 150, 0), {"gap_stop": True}, {}),
+    # round 2: the indirect (CGLS) projection inside solve on a wide problem
+    # (projection.py:152-161): the default tolerance schedule stalls at
+    # MaxIterations, a fixed tolerance converges
+    ("lasso_wide_200x1000_indirect", ("lasso", 200, 1000, 0), {"projection": "indirect"}, {}),
+    ("lasso_wide_200x1000_indirect_ptol", ("lasso", 200, 1000, 0),
+     {"projection": "indirect", "projection_tol": 1e-9}, {}),
+    # Status.DEGENERATE (solver.py:337-342, :414-417): a non-finite prox at
+    # iteration 0 (iterations = 0, the all-zero half iterate is returned) and
+    # a non-finite projection at iteration 0 (iterations = 1, iteration 0's
+    # half iterate is returned)
+    ("degen_prox_300x60", ("degen_prox", 300, 60, 5), {"rho0": 1e10}, {}),
+    ("degen_proj_300x60", ("degen_proj", 300, 60, 5), {}, {}),
 ]
+
+
+def degenerate(kind, m, n, seed):
+    """Lasso-like data with three huge Square targets: b = 1e300 with
+    rho0 = 1e10 overflows the prox of iteration 0; b = 1e308 overflows the
+    over-relaxed projection input of iteration 0 (tests/_cases.py rebuilds it
+    from the stored A and terms)."""
+    rng = np.random.default_rng(seed)
+    A = rng.normal(size=(m, n))
+    b = rng.normal(size=m)
+    b[:3] = 1e300 if kind == "degen_prox" else 1e308
+    f = gf.SeparableFunction.from_arrays(gf.BaseFunction.SQUARE, size=m, b=b)
+    g = gf.SeparableFunction.from_arrays(gf.BaseFunction.ABS, size=n, c=1.0)
+    return gf.GraphFormProblem(A, f, g)
 
 
 def build(desc):
     kind, m, n, seed = desc
+    if kind.startswith("degen_"):
+        return degenerate(kind, m, n, seed)
     if kind == "tall_lasso":
         return tall_lasso(m, n, seed)
     if kind == "tall_lasso32":

@@ -18,6 +18,13 @@ Cases:
   huber_fit_100000x2000_prefix   Huber loss + l1, 60 iterations
                                  (the full solve takes over 30 min on 8 cores)
   entropy_max_2000x50000_prefix  negative entropy, wide (m < n) orientation, 60 iterations
+Round 2 (about 3 hours on 8 cores in total, C3 alone ~90 min):
+  c2_logistic_100000x10000_fixedrho      configs[1], adaptive_rho=False, full solve
+  c2_logistic_100000x10000_fixedrho_r32  the same on fp32-rounded A and terms
+  c2_logistic_100000x10000_prefix200     configs[1], default settings, 200 iterations
+  nnls / basis_pursuit 100000x5000, portfolio 100x200000 (k=100 factors): full solves
+  c3_lp_50000x20000                      configs[2], default settings, full solve
+  entropy_max_2000x50000, huber_fit_100000x2000: full solves
 """
 
 from __future__ import annotations
@@ -45,6 +52,16 @@ CASES = [
     # the other prox kinds and families at scale
     ("huber_fit_100000x2000_prefix", ("huber_fit", 100000, 2000, 0), {"max_iter": 60}),
     ("entropy_max_2000x50000_prefix", ("entropy_max", 2000, 50000, 0), {"max_iter": 60}),
+    # round 2: full solves of configs[1] and configs[2], and the other families at scale
+    ("c2_logistic_100000x10000_fixedrho", ("logistic", 100000, 10000, 0), {"adaptive_rho": False, "max_iter": 1500}),
+    ("c2_logistic_100000x10000_fixedrho_r32", ("logistic32", 100000, 10000, 0), {"adaptive_rho": False, "max_iter": 1500}),
+    ("c2_logistic_100000x10000_prefix200", ("logistic", 100000, 10000, 0), {"max_iter": 200}),
+    ("nnls_100000x5000", ("nnls", 100000, 5000, 0), {}),
+    ("basis_pursuit_100000x5000", ("basis_pursuit", 100000, 5000, 0), {}),
+    ("portfolio_100x200000", ("portfolio", 100, 200000, 0), {}),
+    ("c3_lp_50000x20000", ("lp", 50000, 20000, 0), {}),
+    ("entropy_max_2000x50000", ("entropy_max", 2000, 50000, 0), {}),
+    ("huber_fit_100000x2000", ("huber_fit", 100000, 2000, 0), {}),
 ]
 
 

@@ -34,7 +34,7 @@ def comm(tmp_path_factory):
 def test_one_rank_comm_equals_plain_solve(comm, name):
     fx = _cases.load("solve_" + name)
     prob = _cases.build_problem(fx, as_float32=name.endswith("_r32"))
-    st = gf.SolverSettings(**_cases.settings_of(fx))
+    st = gf.SolverSettings(precision="fp32" if name.endswith("_r32") else None, **_cases.settings_of(fx))
     a = gf.solve(prob, st)
     r0, r1 = distributed.row_range(prob.m, comm.rank, comm.world)
     b = distributed.solve_sharded(prob.A[r0:r1], prob.f.slice(r0, r1), prob.g, st, comm=comm)

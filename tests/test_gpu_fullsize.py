@@ -138,7 +138,7 @@ def test_c5_lasso_200000x5000_fp32():
     fx = fixture("c5_lasso_200000x5000_r32")
     prob = device_instance(fx, fp32=True)
     assert prob.A.dtype == torch.float32
-    st = gf.SolverSettings()
+    st = gf.SolverSettings(precision="fp32")
     res = gf.solve(prob, st)
     it = int(fx["iterations"])
     assert res.status.value == str(fx["status"])
@@ -198,9 +198,9 @@ def test_c2_logistic_100000x10000_prefix():
     _native.convert_matrix(prob.A, A32)
     p32 = gf.GraphFormProblem(A32, prob.f, prob.g)
     del prob
-    r32 = gf.solve(p32, gf.SolverSettings(max_iter=100))
+    r32 = gf.solve(p32, gf.SolverSettings(max_iter=100, precision="fp32"))
     assert r32.iterations <= 100 and np.isfinite(r32.objective)
-    check_properties(p32, r32, gf.SolverSettings(max_iter=100), 2e-3)
+    check_properties(p32, r32, gf.SolverSettings(max_iter=100, precision="fp32"), 2e-3)
 
 
 def test_c3_lp_50000x20000_prefix():

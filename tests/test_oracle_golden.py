@@ -15,9 +15,11 @@ from tests import _cases
 
 def close(a, b, rtol, atol=1e-12):
     """||a-b|| <= rtol*||b|| + atol*sqrt(len): relative for real vectors,
-    absolute for vectors that are zero up to roundoff (e.g. mu when g=Zero)."""
-    a, b = np.asarray(a, float), np.asarray(b, float)
-    return np.linalg.norm(a - b) <= rtol * np.linalg.norm(b) + atol * np.sqrt(b.size)
+    absolute for vectors that are zero up to roundoff (e.g. mu when g=Zero).
+    Vectors holding non-finite or near-overflow entries (degenerate solves)
+    are compared entry by entry: same NaN/inf pattern, finite entries within
+    rtol (see _cases.close_entries)."""
+    return _cases.close_vectors(a, b, rtol, atol)
 
 
 PROX = _cases.load("prox")
@@ -104,7 +106,7 @@ def test_oracle_solve_matches_reference(name):
     np.testing.assert_allclose(res["history"], hist, rtol=1e-8, atol=1e-12)
     for k in ("x", "y", "mu", "nu"):
         assert close(res[k], fx[k], 1e-9), k
-    assert abs(res["objective"] - float(fx["objective"])) <= 1e-9 * max(1, abs(float(fx["objective"])))
+    assert _cases.same_scalar(res["objective"], float(fx["objective"]), 1e-9)
     assert abs(res["final_rho"] - float(fx["final_rho"])) <= 1e-12 * float(fx["final_rho"])
     if "gap" in fx and _cases.settings_of(fx).get("gap_stop"):
         check_gap(res["gap"], fx)

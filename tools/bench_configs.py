@@ -22,6 +22,8 @@ CONFIGS = {
     "c3": ("lp", 50_000, 20_000, np.float64),
     "c4": ("svm", 200_000, 5_000, np.float32),
     "c4d": ("svm", 200_000, 5_000, np.float64),
+    "c5d": ("tall_lasso", 200_000, 5_000, np.float64),
+    "c2d": ("logistic", 100_000, 10_000, np.float64),
 }
 NAMES = ["ginv_gemv_xside", "row_pass_yside", "col_pass", "slab_reduce", "y_scalars", "zstep_controller",
          "allreduce", "fused_rowcol_yside"]
@@ -31,7 +33,10 @@ def run(key, scale=1.0, steps=20):
     fam, m, n, dt = CONFIGS[key]
     m, n = int(m * scale), int(n * scale)
     t0 = time.perf_counter()
-    prob, _ = instances.generate(instances.GenSpec(fam, m, n, 0), device=True)   # A drawn on the GPU
+    if fam == "tall_lasso":
+        prob, _ = instances.tall_lasso(m, n, 0, device=True)
+    else:
+        prob, _ = instances.generate(instances.GenSpec(fam, m, n, 0), device=True)   # A drawn on the GPU
     Ad = prob.A
     if dt == np.float32:
         Ad = instances._dev_matrix(prob.m, prob.n, torch.float32)
@@ -40,14 +45,15 @@ def run(key, scale=1.0, steps=20):
     gen_s = time.perf_counter() - t0
     pd = gf.GraphFormProblem(Ad, prob.f, prob.g)
     A = np.empty((0,), dtype=dt)   # dtype carrier for the byte counts below
+    prec = "fp32" if dt == np.float32 else "fp64"
     setups = []
     for _ in range(2):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        S = gf.prepare(pd)
+        S = gf.prepare(pd, gf.SolverSettings(precision=prec))
         torch.cuda.synchronize()
         setups.append(time.perf_counter() - t0)
-    tight = gf.SolverSettings(abs_tol=1e-14, rel_tol=1e-14, max_iter=3 + 2 * steps + 4)
+    tight = gf.SolverSettings(abs_tol=1e-14, rel_tol=1e-14, max_iter=3 + 2 * steps + 4, precision=prec)
     run_ = slv._Run(S, prob.f, prob.g, tight, None, None, m)
     run_.run(3)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -68,7 +74,7 @@ def run(key, scale=1.0, steps=20):
     # full solve with default settings from the device-resident setup
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    res = gf.solve(pd, gf.SolverSettings(max_iter=2000), setup=S)
+    res = gf.solve(pd, gf.SolverSettings(max_iter=2000, precision=prec), setup=S)
     torch.cuda.synchronize()
     solve_s = time.perf_counter() - t0
     es = A.dtype.itemsize
