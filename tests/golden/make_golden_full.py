@@ -23,6 +23,7 @@ Round 2 (about 3 hours on 8 cores in total, C3 alone ~90 min):
   c2_logistic_100000x10000_fixedrho_r32  the same on fp32-rounded A and terms
   c2_logistic_100000x10000_prefix200     configs[1], default settings, 200 iterations
   nnls / basis_pursuit 100000x5000, portfolio 100x200000 (k=100 factors): full solves
+  lp_5000x2000                           configs[2] at 1/10 scale, full solve (minutes)
   c3_lp_50000x20000                      configs[2], default settings, full solve
   entropy_max_2000x50000, huber_fit_100000x2000: full solves
 """
@@ -59,6 +60,7 @@ CASES = [
     ("nnls_100000x5000", ("nnls", 100000, 5000, 0), {}),
     ("basis_pursuit_100000x5000", ("basis_pursuit", 100000, 5000, 0), {}),
     ("portfolio_100x200000", ("portfolio", 100, 200000, 0), {}),
+    ("lp_5000x2000", ("lp", 5000, 2000, 0), {}),
     ("c3_lp_50000x20000", ("lp", 50000, 20000, 0), {}),
     ("entropy_max_2000x50000", ("entropy_max", 2000, 50000, 0), {}),
     ("huber_fit_100000x2000", ("huber_fit", 100000, 2000, 0), {}),
