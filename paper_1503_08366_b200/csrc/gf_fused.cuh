@@ -32,6 +32,8 @@
 // is issued before the programmatic-dependency wait (A_hat is constant).
 #pragma once
 
+#include <algorithm>
+
 #include "gf_common.cuh"
 #include "gf_gemv.cuh"
 
@@ -367,7 +369,7 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
 #ifdef GF_FUSED_TRACE
       long long c0 = clock64();
 #endif
-      mbar_wait(&redf[b], use & 1u);
+      mbar_wait_u32(smem_u32(&redf[b]), use & 1u);
 #ifdef GF_FUSED_TRACE
       long long c1 = clock64();
       if (lane == 0) GF_TR_ADD(0, c0);
@@ -387,7 +389,7 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
       if (lane == 0) GF_TR_ADD(2, c1);
       c1 = clock64();
 #endif
-      if (use >= 1) mbar_wait(&we[b], (use - 1) & 1u);    // w_s[b] consumed by C(ge-NE)
+      if (use >= 1) mbar_wait_u32(smem_u32(&we[b]), (use - 1) & 1u);    // w_s[b] consumed by C(ge-NE)
 #ifdef GF_FUSED_TRACE
       if (lane == 0) GF_TR_ADD(3, c1);
       c1 = clock64();
@@ -568,24 +570,25 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
 // 20 KB), owns half of the column vectors (half the register state: the
 // 8-warp x 5-vector shape of the fp32 n = 5000 kernel) and writes its
 // half of the column slab.  Per group of TR rows the two CTAs exchange their
-// K = 2 TR partial row dots through distributed shared memory; both then
-// hold the full dots (summed as CTA 0's partial + CTA 1's: identical in
-// both), and row j of the group is finished by CTA (j & 1) only -- its
-// epilogue (prox, duals, stores, reductions) runs once, and its column-pass
-// weights are written into both CTAs' w_s before the arrivals on both wf
-// barriers (count 2: the local and the peer epilogue warp).
+// K = 2 TR partial row dots through distributed shared memory -- the ONLY
+// cross-SM hand-off: both then hold the full dots (summed as CTA 0's partial
+// + CTA 1's, identical in both), both run the pure part of the epilogue
+// (Epi::mid: the column-pass weights) for every row of the group, and row j's
+// stores and reductions (Epi::tail) run in CTA (j & 1) only.  The weights
+// hand-off to the compute warps stays CTA-local.
 //
-// Hand-offs added to the single-CTA pipeline (buffer b = group mod NE):
-//   xbuf[b]  peer's K partial dots, written remotely; xf[b] (count 1) is the
-//            peer's remote arrive.  A partial for use u is sent only after
-//            we[b] of use u-1 completed locally, so the peer can write this
-//            CTA's w_s[b] only once the local compute warps consumed it;
-//            xbuf[b] is free again by then too (the peer's next partial
-//            needs this CTA's wf arrival of use u, made after reading it).
-// Remote writes are st.shared::cluster by lane 0 followed by its
-// mbarrier.arrive.release.cluster; waiters that read remote data use
-// acquire.cluster.  A cluster barrier after the mbarrier init and one before
-// exit keep every remote access inside both CTAs' lifetimes.
+// The exchange uses st.async (asynchronous remote shared-memory stores that
+// complete transaction bytes on the peer's mbarrier): no release fences, so
+// the epilogue warp never waits for its own outstanding global stores (a
+// release.cluster arrive compiles to MEMBAR.ALL.GPU), and the waits on it
+// are CTA-scope (an acquire.cluster wait invalidates L1 every time).
+// Buffers are double-buffered by use parity: xbuf[b][u & 1] / xf[b][u & 1]
+// (count 1: the local arrive.expect_tx of K * 8 bytes; the peer's st.async
+// completes them).  The peer can write use u + 2 only after it has received
+// this CTA's partial of use u + 1, which is sent after use u was read -- so
+// neither the slot nor the barrier phase can be overrun.
+// A cluster barrier after the mbarrier init and one before exit keep every
+// remote access inside both CTAs' lifetimes.
 // ============================================================================
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -621,6 +624,14 @@ __device__ __forceinline__ void mbar_wait_cluster_u32(uint32_t bar, unsigned par
       "@!p bra WAITC_%=;\n\t}" ::"r"(bar),
       "r"(parity), "r"(kSuspendNs)
       : "memory");
+}
+
+// st.async: 8-byte store into a peer CTA's shared memory that completes 8
+// transaction bytes on the peer's mbarrier (both shared::cluster addresses).
+__device__ __forceinline__ void st_async_f64(uint32_t cluster_addr, double v, uint32_t cluster_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(cluster_addr),
+               "d"(v), "r"(cluster_bar)
+               : "memory");
 }
 
 struct FusedPlan2 {
@@ -676,10 +687,10 @@ fused_rowcol_cl2_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const
   static_assert(CW <= 32, "one epilogue lane per compute warp");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxSlots], sfree[kMaxSlots];
-  __shared__ __align__(8) uint64_t redf[NE], rede[NE], wf[NE], we[NE], xf[NE];
+  __shared__ __align__(8) uint64_t redf[NE], rede[NE], wf[NE], we[NE], xf[NE][2];
   __shared__ T red_s[NE][kFusedWarps][K];
   __shared__ __align__(8) T w_s[NE][TR][2];
-  __shared__ __align__(8) double xbuf[NE][K];
+  __shared__ __align__(8) double xbuf[NE][2][K];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t rank = cluster_ctarank(), peer = rank ^ 1u;
@@ -702,9 +713,10 @@ fused_rowcol_cl2_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const
     for (int b = 0; b < NE; ++b) {
       mbar_init(&redf[b], kFusedWarps);
       mbar_init(&rede[b], 1);
-      mbar_init(&wf[b], 2);
+      mbar_init(&wf[b], 1);
       mbar_init(&we[b], kFusedWarps);
-      mbar_init(&xf[b], 1);
+      mbar_init(&xf[b][0], 1);
+      mbar_init(&xf[b][1], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -746,16 +758,14 @@ fused_rowcol_cl2_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const
 #pragma unroll
       for (int k = 0; k < (NR > 0 ? NR : 1); ++k) ered[k] = 0.0;
       unsigned eflags = 0;
-      const uint32_t xb_peer = mapa_u32(smem_u32(&xbuf[b][0]), peer);
-      const uint32_t xf_peer = mapa_u32(smem_u32(&xf[b]), peer);
-      const uint32_t wf_peer = mapa_u32(smem_u32(&wf[b]), peer);
-      const uint32_t ws_peer = mapa_u32(smem_u32(&w_s[b][0][0]), peer);
-      const uint32_t xf_loc = smem_u32(&xf[b]);
+      const uint32_t xb_peer = mapa_u32(smem_u32(&xbuf[b][0][0]), peer);
+      const uint32_t xf_peer = mapa_u32(smem_u32(&xf[b][0]), peer);
+      const uint32_t xf_loc = smem_u32(&xf[b][0]), we_loc = smem_u32(&we[b]), redf_loc = smem_u32(&redf[b]);
       typename Epi::RowIn in{};
       if (lane < TR && par * TR + lane < nr) in = epi.load_in(r0 + par * TR + lane);
       for (int ge = par; ge < ng; ge += NE) {
-        const unsigned use = (unsigned)(ge / NE);
-        mbar_wait(&redf[b], use & 1u);
+        const unsigned use = (unsigned)(ge / NE), p = use & 1u;
+        mbar_wait_u32(redf_loc, use & 1u);
         constexpr int RW = CW <= 16 ? 16 : 32;
         double v[K];
 #pragma unroll
@@ -766,44 +776,34 @@ fused_rowcol_cl2_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const
         for (int q = 0; q < K; ++q)
 #pragma unroll
           for (int o = RW / 2; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o, RW);
-        if (use >= 1) mbar_wait(&we[b], (use - 1) & 1u);    // local w_s[b] consumed by C(ge - NE)
-        // this CTA's partials -> the peer
-        if (lane == 0) {
+        // this CTA's partials -> the peer's xbuf[b][p] (lane q sends value q)
 #pragma unroll
-          for (int q = 0; q < K; ++q) st_cluster_f64(xb_peer + 8u * q, v[q]);
-          mbar_arrive_remote(xf_peer);
-        }
-        mbar_wait_cluster_u32(xf_loc, use & 1u);           // the peer's partials
+        for (int q = 0; q < K; ++q)
+          if (lane == q) st_async_f64(xb_peer + 8u * (unsigned)(p * K + q), v[q], xf_peer + 8u * p);
+        if (lane == 0) mbar_arrive_expect_tx(&xf[b][p], (unsigned)(K * sizeof(double)));
+        mbar_wait_u32(xf_loc + 8u * p, (use >> 1) & 1u);   // the peer's partials have landed
         const int g = min(TR, nr - ge * TR);
         double dots[2] = {0.0, 0.0};
 #pragma unroll
         for (int rr = 0; rr < TR; ++rr)
           if (rr == lane) {
-            const double p0 = xbuf[b][2 * rr], p1 = xbuf[b][2 * rr + 1];
+            const double p0 = xbuf[b][p][2 * rr], p1 = xbuf[b][p][2 * rr + 1];
             dots[0] = rank == 0 ? v[2 * rr] + p0 : p0 + v[2 * rr];
             dots[1] = rank == 0 ? v[2 * rr + 1] + p1 : p1 + v[2 * rr + 1];
           }
+        // every row's weights are computed here (mid is pure: both CTAs get
+        // the same values); tail() only for this CTA's rows
         const bool mine = lane < g && (((ge * TR + lane) & 1) == (int)rank);
         typename Epi::Mid md{};
         double w0 = 0.0, w1 = 0.0;
-        if (mine) md = epi.mid(in, dots, w0, w1);
-        // lane 0 writes the weights of this CTA's rows into both CTAs' w_s
-        // and arrives on both wf[b]
-#pragma unroll
-        for (int rr = 0; rr < TR; ++rr) {
-          const double a0 = __shfl_sync(0xffffffffu, w0, rr);
-          const double a1 = __shfl_sync(0xffffffffu, w1, rr);
-          if (lane == 0 && rr < g && (((ge * TR + rr) & 1) == (int)rank)) {
-            w_s[b][rr][0] = (T)a0;
-            w_s[b][rr][1] = (T)a1;
-            st_cluster(ws_peer + (unsigned)((rr * 2) * sizeof(T)), (T)a0);
-            st_cluster(ws_peer + (unsigned)((rr * 2 + 1) * sizeof(T)), (T)a1);
-          }
+        if (lane < g) md = epi.mid(in, dots, w0, w1);
+        if (use >= 1) mbar_wait_u32(we_loc, (use - 1) & 1u);    // w_s[b] consumed by C(ge - NE)
+        if (lane < g) {
+          w_s[b][lane][0] = (T)w0;
+          w_s[b][lane][1] = (T)w1;
         }
-        if (lane == 0) {
-          mbar_arrive_remote(wf_peer);
-          mbar_arrive_expect_tx(&wf[b], 0);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(&wf[b], 0);
         if (mine) epi.tail(r0 + (int64_t)ge * TR + lane, in, dots, md, ered, eflags);
         const int jn = (ge + NE) * TR + lane;
         if (lane < TR && jn < nr) in = epi.load_in(r0 + jn);
@@ -885,7 +885,7 @@ fused_rowcol_cl2_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const
           if (++bR == NE) { bR = 0; ++useR; }
         }
         if (t >= 2) {   // ---- C(t-2) ----
-          mbar_wait_cluster_u32(wf0 + 8u * bC, useC & 1u);   // weights partly written by the peer
+          mbar_wait_u32(wf0 + 8u * bC, useC & 1u);
           T w0[TR], w1[TR];
 #pragma unroll
           for (int rr = 0; rr < TR; ++rr) { w0[rr] = w_s[bC][rr][0]; w1[rr] = w_s[bC][rr][1]; }

@@ -137,6 +137,9 @@ void eval_base(int kind, int64_t n, const double* x, double* out, cudaStream_t s
 void conj_base(int kind, int64_t n, const double* w, double* out, cudaStream_t st);
 double conjugate(const TermsView& t, int64_t n, const double* w, bool* supported, cudaStream_t st);
 bool conj_supported(const TermsView& t, int64_t n, cudaStream_t st);
+// true if any term's (effective) kind is one whose prox is an iterative
+// Newton solve (NegEntr, Logistic): variable, up to 100-step epilogues
+bool has_newton_prox(const TermsView& t, int64_t n, cudaStream_t st);
 
 // ------------------------------------------------- CGLS indirect (gf_cgls) --
 int64_t cgls_solve(const gf_matrix* A, bool tall, gf_comm* comm, const double* h1, const double* h2, double* z,

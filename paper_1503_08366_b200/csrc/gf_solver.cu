@@ -1563,9 +1563,16 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
     // (gf_fused.cuh, fused_rowcol_cl2_kernel) -- half the bytes per slot,
     // two rows per group, half the column state per CTA.  GF_FUSED_CL2=0
     // disables it, =1 forces it for any tall shape (measurements).
+    // Not for Newton-prox losses (logistic, negative entropy): one row's prox
+    // can take up to 100 Newton steps, and in the single pass every such row
+    // stalls its cluster's whole stream, while the two-pass row pass runs the
+    // epilogues 32 rows per warp over thousands of warps (measured C2
+    // logistic 100000 x 10000 fp32: 1.35 ms cluster pass vs 1.33 two-pass).
     const char* cl2env = getenv("GF_FUSED_CL2");
     const bool cl2_off = cl2env && cl2env[0] == '0', cl2_force = cl2env && cl2env[0] == '1';
-    if (s->tall && !cl2_off && (cl2_force || (one_row && !s->fplan.ok)) &&
+    const bool newton = s->tall && !cl2_force && !cl2_off && one_row && !s->fplan.ok &&
+                        has_newton_prox(s->f.view, s->m, st);
+    if (s->tall && !cl2_off && !newton && (cl2_force || (one_row && !s->fplan.ok)) &&
         !(env && env[0] == '1')) {
       s->fplan2 = plan_fused_cl2(s->m, s->ld, (int)es, sms, (size_t)optin, sms / 2);
       if (s->fplan2.ok && (s->fplan2.tr >= 2 || cl2_force)) {

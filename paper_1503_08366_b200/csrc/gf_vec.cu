@@ -138,6 +138,25 @@ bool conj_supported(const TermsView& t, int64_t n, cudaStream_t st) {
   return u == 0;
 }
 
+__global__ void newton_kind_kernel(TermsView t, int64_t n, unsigned* __restrict__ hit) {
+  for (int64_t i = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const Term u = load_term(t, i);
+    if (u.c != 0.0 && (u.h == kLogistic || u.h == kNegEntr)) atomicOr(hit, 1u);
+  }
+}
+
+bool has_newton_prox(const TermsView& t, int64_t n, cudaStream_t st) {
+  if (n <= 0) return false;
+  DBuf flag(sizeof(unsigned));
+  GF_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(unsigned), st));
+  newton_kind_kernel<<<egrid(n), 256, 0, st>>>(t, n, flag.as<unsigned>());
+  GF_CHECK_LAUNCH();
+  unsigned u = 0;
+  GF_CUDA(cudaMemcpyAsync(&u, flag.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  GF_CUDA(cudaStreamSynchronize(st));
+  return u != 0;
+}
+
 void conj_base(int kind, int64_t n, const double* w, double* out, cudaStream_t st) {
   if (n <= 0) return;
   conj_base_kernel<<<egrid(n), 256, 0, st>>>(kind, n, w, out);
