@@ -184,7 +184,7 @@ struct FusedPlan {
   bool ok = false;
 };
 
-inline FusedPlan plan_fused(int64_t m, int64_t ld, int esize, int sms, size_t smem_max) {
+inline FusedPlan plan_fused(int64_t m, int64_t ld, int esize, int sms, size_t smem_max, int max_slots = kMaxSlots) {
   FusedPlan p;
   const int vn = 16 / esize;
   const int64_t nvec = ld / vn;
@@ -201,7 +201,7 @@ inline FusedPlan plan_fused(int64_t m, int64_t ld, int esize, int sms, size_t sm
   p.ne = fused_epi(p.cw);
   const size_t row_bytes = (size_t)ld * esize;
   const size_t budget = smem_max > 8192 ? smem_max - 8192 : 0;
-  p.nslot = (int)std::min<size_t>(kMaxSlots, budget / row_bytes);
+  p.nslot = (int)std::min<size_t>(std::min(max_slots, kMaxSlots), budget / row_bytes);
   // keep >= 2 rows and >= 48 KB of TMA prefetch beyond the three resident groups
   const int want_pf = std::max<int>(2, (int)ceil_div(48 * 1024, (int64_t)row_bytes));
   p.tr = 0;
@@ -645,7 +645,8 @@ struct FusedPlan2 {
 // max_clusters: co-resident 2-CTA clusters at this shared-memory size
 // (cudaOccupancyMaxActiveClusters): the kernel is persistent, every cluster
 // must be resident in one wave.
-inline FusedPlan2 plan_fused_cl2(int64_t m, int64_t ld, int esize, int sms, size_t smem_max, int max_clusters) {
+inline FusedPlan2 plan_fused_cl2(int64_t m, int64_t ld, int esize, int sms, size_t smem_max, int max_clusters,
+                                 int max_slots = kMaxSlots) {
   FusedPlan2 p;
   const int vn = 16 / esize;
   const int64_t nvec = ld / vn;
@@ -657,7 +658,7 @@ inline FusedPlan2 plan_fused_cl2(int64_t m, int64_t ld, int esize, int sms, size
   p.ne = fused_epi(p.cw);
   const size_t slot_bytes = (size_t)p.hvec * 16;
   const size_t budget = smem_max > 8192 ? smem_max - 8192 : 0;
-  p.nslot = (int)std::min<size_t>(kMaxSlots, budget / slot_bytes);
+  p.nslot = (int)std::min<size_t>(std::min(max_slots, kMaxSlots), budget / slot_bytes);
   const int want_pf = std::max<int>(2, (int)ceil_div(48 * 1024, (int64_t)slot_bytes));
   p.tr = 0;
   for (int tr : {4, 2, 1})

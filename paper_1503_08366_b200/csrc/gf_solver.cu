@@ -1543,7 +1543,12 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
       if (s->dtype == GF_F32) ring_dispatch<float>(s.get(), nullptr, true);
       else ring_dispatch<double>(s.get(), nullptr, true);
     }
-    s->fplan = plan_fused(s->m, s->ld, (int)es, sms, (size_t)optin);
+    // GF_FUSED_MAXSLOTS (dev): cap the ring slots -- compute-sanitizer's
+    // synccheck tracks a bounded number of mbarriers per CTA
+    // (tools/san/mbar_sanity.cu), so its runs use small rings
+    const char* ms_env = getenv("GF_FUSED_MAXSLOTS");
+    const int max_slots = ms_env ? std::max(4, atoi(ms_env)) : kMaxSlots;
+    s->fplan = plan_fused(s->m, s->ld, (int)es, sms, (size_t)optin, max_slots);
     const char* env = getenv("GF_DISABLE_FUSED");
     if ((env && env[0] == '1') || !s->tall) s->fplan.ok = false;
     // With only one row per group (rows of ~40 KB and more: five ring slots)
@@ -1574,11 +1579,11 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
                         has_newton_prox(s->f.view, s->m, st);
     if (s->tall && !cl2_off && !newton && (cl2_force || (one_row && !s->fplan.ok)) &&
         !(env && env[0] == '1')) {
-      s->fplan2 = plan_fused_cl2(s->m, s->ld, (int)es, sms, (size_t)optin, sms / 2);
+      s->fplan2 = plan_fused_cl2(s->m, s->ld, (int)es, sms, (size_t)optin, sms / 2, max_slots);
       if (s->fplan2.ok && (s->fplan2.tr >= 2 || cl2_force)) {
         const int ncl = s->dtype == GF_F32 ? fused2_dispatch<float>(s.get(), nullptr, true)
                                            : fused2_dispatch<double>(s.get(), nullptr, true);
-        s->fplan2 = plan_fused_cl2(s->m, s->ld, (int)es, sms, (size_t)optin, ncl);
+        s->fplan2 = plan_fused_cl2(s->m, s->ld, (int)es, sms, (size_t)optin, ncl, max_slots);
         if (s->fplan2.ok) s->fplan.ok = false;
       } else {
         s->fplan2.ok = false;
