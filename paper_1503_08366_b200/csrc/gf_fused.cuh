@@ -40,6 +40,9 @@
 namespace gf {
 
 constexpr int kMaxSlots = 32;
+// static shared memory of the kernels (barriers, hand-off buffers, the Z
+// tail's reduction scratch) comes out of the same per-block limit as the ring
+constexpr size_t kStaticSmemReserve = 16384;
 // Epilogue warps: warp e takes the groups ge = e (mod kFusedEpi) and owns
 // hand-off buffer e, so each warp has kFusedEpi row-pass periods per group
 // while the latency from R(ge) to its weights stays under the two-period lag.
@@ -200,7 +203,7 @@ inline FusedPlan plan_fused(int64_t m, int64_t ld, int esize, int sms, size_t sm
   p.nv = (int)ceil_div(nvec, p.cw * 32);
   p.ne = fused_epi(p.cw);
   const size_t row_bytes = (size_t)ld * esize;
-  const size_t budget = smem_max > 8192 ? smem_max - 8192 : 0;
+  const size_t budget = smem_max > kStaticSmemReserve ? smem_max - kStaticSmemReserve : 0;
   p.nslot = (int)std::min<size_t>(std::min(max_slots, kMaxSlots), budget / row_bytes);
   // keep >= 2 rows and >= 48 KB of TMA prefetch beyond the three resident groups
   const int want_pf = std::max<int>(2, (int)ceil_div(48 * 1024, (int64_t)row_bytes));
@@ -244,6 +247,13 @@ __device__ __forceinline__ T warp_multi_sum(T (&v)[K], int lane) {
   return r;
 }
 
+// Work run by every thread of every CTA after the pass (the solver's Z step,
+// ZTail in gf_solver.cu); NoTail: none.
+struct NoTail {
+  __device__ bool on() const { return false; }
+  __device__ void run() const {}
+};
+
 // Epi must provide: NR, active(), begin(), RowIn, load_in(i), Mid,
 // mid(in, dots, w0, w1) (the column-pass weights: critical path) and
 // tail(i, in, dots, mid, red, flags) (stores, reductions)  -- YEpi does.
@@ -270,11 +280,11 @@ __device__ unsigned long long gf_fused_trace[148 * 16];
 #define GF_TR_ADD(slot, t0) (void)0
 #endif
 
-template <typename T, int NV, int TR, int CW, class Epi>
+template <typename T, int NV, int TR, int CW, class Epi, class Tail = NoTail>
 __global__ void __launch_bounds__(fused_threads(CW), 1)
 fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* __restrict__ x0,
                     const T* __restrict__ x1, Epi epi, int nslot, double* __restrict__ rpart,
-                    double* __restrict__ cpart) {
+                    double* __restrict__ cpart, Tail tail = Tail{}) {
   using V = typename Vec16<T>::type;
   constexpr int VN = Vec16<T>::n;
   constexpr int NR = Epi::NR;
@@ -348,9 +358,7 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
         if (++slot == nslot) slot = 0;
       }
     }
-    return;
-  }
-
+  } else {
   pdl_wait();
   if (!epi.active()) return;
   if (warp >= kEpiWarp && warp < kEpiWarp + NE) {
@@ -431,8 +439,7 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
       for (int k = 0; k < NR; ++k) out[k] = ered[k];
       out[NR] = (double)eflags;
     }
-    return;
-  }
+  } else {
 
   // ===================== compute warps =====================
   // Thread tid owns the 16-byte column vectors c = tid + v * CW * 32.  Only
@@ -557,6 +564,11 @@ fused_rowcol_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* 
       }
     }
   }
+  }   // compute warps
+  }   // consumer warps
+  // every thread of an active CTA arrives here (the producer warp too; when
+  // the solve has ended every CTA skips the tail alike)
+  if (tail.on() && epi.active()) tail.run();
 }
 
 
@@ -657,7 +669,7 @@ inline FusedPlan2 plan_fused_cl2(int64_t m, int64_t ld, int esize, int sms, size
   p.nv = (int)ceil_div(p.hvec, p.cw * 32);
   p.ne = fused_epi(p.cw);
   const size_t slot_bytes = (size_t)p.hvec * 16;
-  const size_t budget = smem_max > 8192 ? smem_max - 8192 : 0;
+  const size_t budget = smem_max > kStaticSmemReserve ? smem_max - kStaticSmemReserve : 0;
   p.nslot = (int)std::min<size_t>(std::min(max_slots, kMaxSlots), budget / slot_bytes);
   const int want_pf = std::max<int>(2, (int)ceil_div(48 * 1024, (int64_t)slot_bytes));
   p.tr = 0;
@@ -670,11 +682,11 @@ inline FusedPlan2 plan_fused_cl2(int64_t m, int64_t ld, int esize, int sms, size
   return p;
 }
 
-template <typename T, int NV, int TR, int CW, class Epi>
+template <typename T, int NV, int TR, int CW, class Epi, class Tail = NoTail>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fused_threads(CW), 1)
 fused_rowcol_cl2_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* __restrict__ x0,
                         const T* __restrict__ x1, Epi epi, int nslot, int64_t hvec, double* __restrict__ rpart,
-                        double* __restrict__ cpart) {
+                        double* __restrict__ cpart, Tail tail = Tail{}) {
   using V = typename Vec16<T>::type;
   constexpr int VN = Vec16<T>::n;
   constexpr int NR = Epi::NR;
@@ -929,6 +941,7 @@ fused_rowcol_cl2_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const
   }
   __syncthreads();
   cluster_sync_all();   // no CTA leaves while its peer may still access its shared memory
+  if (tail.on() && epi.active()) tail.run();
 }
 
 }  // namespace gf

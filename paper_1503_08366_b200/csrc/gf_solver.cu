@@ -55,6 +55,7 @@ struct Ctl {
   double r_pri, r_dual, eps_pri, eps_dual, objective;
   double gap;          // duality gap of the last gap test (solver.py:378-390)
   int64_t gap_set;     // 1 once a gap was computed
+  unsigned gcnt, ggen; // grid barrier of the fused pass's Z tail (arrivals, generation)
 };
 
 struct Params {
@@ -868,6 +869,229 @@ zslab_tall_kernel(Ctl* __restrict__ ctl, Params prm, const double* __restrict__ 
   decide_tall(ctl, prm, ys, xs, r2, hist);
 }
 
+// --------------------------------------------- Z step in the fused pass --
+// The fused schedules end with the Z step inside the same launch (ZTail, run
+// by every thread of every CTA after the main loop; the pass is persistent:
+// one CTA per SM, all co-resident, so a grid barrier is safe):
+//   barrier -> CTA b sums the slabs of columns [n b / G, n (b+1) / G) in
+//              fixed slab order; CTA 0 the y records
+//   mode 2 (one GPU): rhs = c_x + A' c_y and the r_dual^2 partial of those
+//              columns at once, CTA 0's x records, and the controller in the
+//              last CTA to arrive (ticket) -- one barrier, no second launch
+//   mode 1 (row partition): the column sums and y scalars go to red, which is
+//              all-reduced; zfinish_kernel then finishes the same columns in
+//              the same lane order with the same grid, so one rank is
+//              bit-identical to the communicator-free path.
+// This replaces the separate Z launch (slab sums + controller: ~20 us at
+// 200000 x 5000, most of it launch ramp and the serial tail).
+__device__ __forceinline__ void grid_sync(unsigned* cnt, unsigned* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vg = gen;
+    const unsigned g0 = *vg;
+    __threadfence();
+    if (atomicAdd(cnt, 1u) == gridDim.x - 1) {
+      atomicExch(cnt, 0u);
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*vg == g0) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+constexpr int kTailThreads = 256;   // threads of a CTA that do the Z work (fixed: same sums in both modes)
+constexpr int kTailSlabs = 20;      // slab loads in flight per lane (per warp: slabs w, w + 8, ...)
+
+template <typename T>
+struct ZTail {
+  Ctl* ctl;
+  Params prm;
+  const double* cpart;
+  int64_t slabs, ld, n;
+  const double* rpart;
+  int64_t nrpart;
+  const double* cx;
+  const double* e;
+  const double* muh2;
+  T* rhs_T;
+  double* zpart;
+  const double* xpart;
+  int64_t nxpart;
+  double* hist;
+  double* red;   // [2 ld column sums | kScal y scalars | kRedX + 1 x sums]
+  int mode;      // 0 off, 1 column sums + y scalars only, 2 the whole Z step
+
+  __device__ bool on() const { return mode != 0; }
+
+  // Columns [n b / G, n (b+1) / G) of CTA b, 32 at a time: warp w < 8 loads
+  // slabs w, w + 8, ... of both sums (all loads issued before the adds), a
+  // fixed-order combine over the 8 warps in shared memory, then warp 0's lane
+  // l holds column cc + l: mode 1 stores it in red, mode 2 finishes it.
+  __device__ void run() const {
+    grid_sync(&ctl->gcnt, &ctl->ggen);
+    __shared__ double part[8][2][33];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool act = tid < kTailThreads;
+    const int64_t G = gridDim.x, b = blockIdx.x;
+    const int64_t c0 = n * b / G, c1 = n * (b + 1) / G;
+    const double* muh = muh2 + (ctl->k & 1) * n;
+    double rd2 = 0.0;
+    for (int64_t cc = c0; cc < c1; cc += 32) {   // uniform trip count in the CTA
+      const int64_t j = cc + lane;
+      double s1 = 0.0, s2 = 0.0;
+      if (act && j < c1) {
+        for (int64_t sb = warp; sb < slabs; sb += 8 * kTailSlabs) {
+          double v1[kTailSlabs], v2[kTailSlabs];
+#pragma unroll
+          for (int u = 0; u < kTailSlabs; ++u) {
+            const int64_t sl = sb + 8 * u;
+            v1[u] = sl < slabs ? cpart[(2 * sl) * ld + j] : 0.0;
+            v2[u] = sl < slabs ? cpart[(2 * sl + 1) * ld + j] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < kTailSlabs; ++u) { s1 += v1[u]; s2 += v2[u]; }
+        }
+      }
+      if (act) {
+        part[warp][0][lane] = s1;
+        part[warp][1][lane] = s2;
+      }
+      __syncthreads();
+      if (warp == 0 && j < c1) {
+        double t1 = part[0][0][lane], t2 = part[0][1][lane];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) { t1 += part[w][0][lane]; t2 += part[w][1][lane]; }
+        if (mode == 1) {
+          red[j] = t1;
+          red[ld + j] = t2;
+        } else {
+          rd2 += column(j, t1, t2, muh);
+        }
+      }
+      __syncthreads();
+    }
+    if (b == 0) y_records();
+    if (mode == 2) close(rd2);
+  }
+
+  // rhs_j = c_x,j + (A_hat' c_y)_j (projection.py:121); returns the r_dual
+  // term ((A' nu + mu)_j in the original space)^2
+  __device__ double column(int64_t j, double s1, double s2, const double* muh) const {
+    rhs_T[j] = (T)A_(cx[j], s1);
+    const double ej = e[j];
+    const double rdj = A_(D_(s2, ej), D_(muh[j], ej));
+    return rdj * rdj;
+  }
+
+  // y records (rpart) -> the controller's scalar layout at red + 2 ld
+  __device__ void y_records() const {
+    __shared__ double shr[8][kRedY + 1];
+    double yr[kRedY + 1];
+    block_records<kRedY>(rpart, nrpart, yr, shr);
+    if (threadIdx.x == 0) y_layout(yr, red + 2 * ld);
+  }
+
+  // fixed-order sums of `count` records of K values + a flags word, over the
+  // first kTailThreads threads; thread 0 gets the result
+  template <int K>
+  __device__ void block_records(const double* rec, int64_t count, double (&out)[K + 1], double (*sh)[K + 1]) const {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool act = tid < kTailThreads;
+    double v[K + 1];
+#pragma unroll
+    for (int q = 0; q <= K; ++q) v[q] = 0.0;
+    unsigned fl = 0;
+    if (act)
+      for (int64_t i = tid; i < count; i += kTailThreads) {
+#pragma unroll
+        for (int q = 0; q < K; ++q) v[q] += rec[i * (K + 1) + q];
+        fl |= (unsigned)rec[i * (K + 1) + K];
+      }
+#pragma unroll
+    for (int q = 0; q < K; ++q) v[q] = warp_sum(v[q]);
+    fl = warp_or(fl);
+    if (act && lane == 0) {
+#pragma unroll
+      for (int q = 0; q < K; ++q) sh[warp][q] = v[q];
+      sh[warp][K] = (double)fl;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned f = 0;
+      for (int q = 0; q < K; ++q) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += sh[w][q];
+        out[q] = t;
+      }
+      for (int w = 0; w < 8; ++w) f |= (unsigned)sh[w][K];
+      out[K] = (double)f;
+    }
+    __syncthreads();
+  }
+
+  // this CTA's r_dual^2 partial (held by warp 0's lanes), CTA 0's x records,
+  // then the controller in the last CTA to arrive
+  __device__ void close(double rd2) const {
+    __shared__ double shx[8][kRedX + 1];
+    __shared__ bool last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t G = gridDim.x, b = blockIdx.x;
+    double* xs = red + 2 * ld + kScal;
+    if (b == 0) {
+      double xr[kRedX + 1];
+      block_records<kRedX>(xpart, nxpart, xr, shx);
+      if (tid == 0)
+        for (int q = 0; q <= kRedX; ++q) xs[q] = xr[q];
+    }
+    if (warp == 0) {
+      rd2 = warp_sum(rd2);
+      if (lane == 0) {
+        zpart[b] = rd2;
+        __threadfence();
+        last = atomicAdd(&ctl->ticket, 1u) == (unsigned)G - 1;
+      }
+    }
+    __syncthreads();
+    if (!last || warp != 0) return;
+    __threadfence();
+    double z = 0.0;   // fixed order: lane l sums CTAs l, l + 32, ...; then a fixed tree
+    for (int64_t i = lane; i < G; i += 32) z += ((volatile const double*)zpart)[i];
+    z = warp_sum(z);
+    if (lane != 0) return;
+    ctl->ticket = 0;
+    decide_tall(ctl, prm, red + 2 * ld, xs, z, hist);
+  }
+
+  // mode 1's second half, after the all-reduce of red: the same columns in
+  // the same lane order as run()'s mode 2, then close()
+  __device__ void finish() const {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t G = gridDim.x, b = blockIdx.x;
+    const int64_t c0 = n * b / G, c1 = n * (b + 1) / G;
+    const double* muh = muh2 + (ctl->k & 1) * n;
+    double rd2 = 0.0;
+    if (warp == 0)
+      for (int64_t cc = c0; cc < c1; cc += 32) {
+        const int64_t j = cc + lane;
+        if (j < c1) rd2 += column(j, red[j], red[ld + j], muh);
+      }
+    (void)tid;
+    close(rd2);
+  }
+};
+
+// Row-partitioned fused schedules: finish() after the all-reduce of red, with
+// the fused pass's grid (same column partition: one rank is bit-identical to
+// the single-GPU in-kernel Z step).
+template <typename T>
+__global__ void __launch_bounds__(kTailThreads) zfinish_kernel(ZTail<T> z) {
+  if (z.ctl->status != GF_STATUS_RUNNING) return;
+  z.finish();
+}
+
 // ------------------------------------------------------------- results --
 __global__ void result_kernel(const Ctl* ctl, int64_t n, int64_t m, const double* __restrict__ xh2,
                               const double* __restrict__ muh2, const double* __restrict__ yh2,
@@ -1058,17 +1282,44 @@ static bool use_pdl(const gf_solver* s) {
 }
 
 // attr_only: set the dynamic shared-memory limit of the instance (at create)
+// The Z step carried by the fused pass: mode 2 on one GPU (whole step in
+// the launch), mode 1 under a communicator (column sums + y scalars; the
+// all-reduce and zfinish_kernel follow).
+template <typename T>
+static ZTail<T> make_ztail(gf_solver* s, int64_t slabs, int64_t nrpart) {
+  ZTail<T> z;
+  z.ctl = s->ctl.as<Ctl>();
+  z.prm = s->prm;
+  z.cpart = s->cpart.as<double>();
+  z.slabs = slabs;
+  z.ld = s->ld;
+  z.n = s->n;
+  z.rpart = s->rpart.as<double>();
+  z.nrpart = nrpart;
+  z.cx = s->cx.as<double>();
+  z.e = s->S->e.as<double>();
+  z.muh2 = s->muh2.as<double>();
+  z.rhs_T = s->rhs_T.as<T>();
+  z.zpart = s->zpart.as<double>();
+  z.xpart = s->xpart.as<double>();
+  z.nxpart = s->grid_s;
+  z.hist = s->hist.as<double>();
+  z.red = s->red.as<double>();
+  z.mode = comm_active(s->S->comm) ? 1 : 2;
+  return z;
+}
+
 template <typename T, int NV, int TR, int CW>
 static void fused_go(gf_solver* s, cudaStream_t st, bool attr_only) {
   const FusedPlan& p = s->fplan;
-  auto kern = fused_rowcol_kernel<T, NV, TR, CW, YEpi<T>>;
+  auto kern = fused_rowcol_kernel<T, NV, TR, CW, YEpi<T>, ZTail<T>>;
   if (attr_only) {
     GF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
     return;
   }
   launch_k(use_pdl(s), kern, dim3(p.grid), dim3(fused_threads(CW)), p.smem, st, (const T*)s->S->A->data, s->m,
            s->ld, (const T*)s->xk_T.as<T>(), (const T*)s->xh_T.as<T>(), make_yepi<T>(s), p.nslot,
-           s->rpart.as<double>(), s->cpart.as<double>());
+           s->rpart.as<double>(), s->cpart.as<double>(), make_ztail<T>(s, p.grid, (int64_t)p.ne * p.grid));
   GF_CHECK_LAUNCH();
 }
 
@@ -1117,7 +1368,7 @@ static void fused_dispatch(gf_solver* s, cudaStream_t st, bool attr_only) {
 template <typename T, int NV, int TR, int CW>
 static int fused2_go(gf_solver* s, cudaStream_t st, bool attr_only) {
   const FusedPlan2& p = s->fplan2;
-  auto kern = fused_rowcol_cl2_kernel<T, NV, TR, CW, YEpi<T>>;
+  auto kern = fused_rowcol_cl2_kernel<T, NV, TR, CW, YEpi<T>, ZTail<T>>;
   if (attr_only) {
     GF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
     cudaLaunchConfig_t cfg = {};
@@ -1130,7 +1381,7 @@ static int fused2_go(gf_solver* s, cudaStream_t st, bool attr_only) {
   }
   launch_k(use_pdl(s), kern, dim3(p.grid), dim3(fused_threads(CW)), p.smem, st, (const T*)s->S->A->data, s->m,
            s->ld, (const T*)s->xk_T.as<T>(), (const T*)s->xh_T.as<T>(), make_yepi<T>(s), p.nslot, p.hvec,
-           s->rpart.as<double>(), s->cpart.as<double>());
+           s->rpart.as<double>(), s->cpart.as<double>(), make_ztail<T>(s, p.grid / 2, (int64_t)p.ne * p.grid));
   GF_CHECK_LAUNCH();
   return 0;
 }
@@ -1269,23 +1520,32 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
     s->mark(0, st, false);
     s->launches += 1;
   }
+  if (s->m > 0 && (s->fplan.ok || s->fplan2.ok)) {
+    // one pass over A_hat (row pass + y side + column pass) carrying the Z
+    // step: alone on one GPU; under a communicator the column sums and y
+    // scalars, then the all-reduce and the rest of the Z step
+    s->mark(7, st, true);
+    if (s->fplan.ok) launch_fused<T>(s, st);
+    else fused2_dispatch<T>(s, st, false);   // rows split over 2-CTA clusters
+    s->mark(7, st, false);
+    s->launches += 1;
+    if (!comm_active(s->S->comm)) return;
+    s->mark(6, st, true);
+    allreduce_sum(s->S->comm, s->red.as<double>(), 2 * s->ld + kScal, st);
+    s->mark(6, st, false);
+    s->mark(5, st, true);
+    const unsigned g = (unsigned)(s->fplan.ok ? s->fplan.grid : s->fplan2.grid);
+    const int64_t slabs = s->fplan.ok ? s->fplan.grid : s->fplan2.grid / 2;
+    const int64_t nrpart = s->fplan.ok ? (int64_t)s->fplan.ne * s->fplan.grid : (int64_t)s->fplan2.ne * s->fplan2.grid;
+    zfinish_kernel<T><<<g, kTailThreads, 0, st>>>(make_ztail<T>(s, slabs, nrpart));
+    GF_CHECK_LAUNCH();
+    s->mark(5, st, false);
+    s->launches += 1;
+    return;
+  }
   if (s->m > 0) {
     int64_t slabs, nrpart;
-    if (s->fplan.ok) {   // one pass over A_hat: row pass + y side + column pass
-      s->mark(7, st, true);
-      launch_fused<T>(s, st);
-      s->mark(7, st, false);
-      slabs = s->fplan.grid;
-      nrpart = s->fplan.ne * s->fplan.grid;   // one record per epilogue warp
-      s->launches += 1;
-    } else if (s->fplan2.ok) {   // the same single pass, rows split over 2-CTA clusters
-      s->mark(7, st, true);
-      fused2_dispatch<T>(s, st, false);
-      s->mark(7, st, false);
-      slabs = s->fplan2.grid / 2;              // one slab per cluster
-      nrpart = s->fplan2.ne * s->fplan2.grid;
-      s->launches += 1;
-    } else {             // two passes: row pass (+ y side), then column pass
+    {             // two passes: row pass (+ y side), then column pass
       s->mark(1, st, true);
       rowgemv_kernel<T, 2, YEpi<T>><<<(unsigned)s->grid_r, kRowThreads, 0, st>>>(
           (const T*)A->data, s->m, s->ld, s->xk_T.as<T>(), s->xh_T.as<T>(), make_yepi<T>(s), s->rpart.as<double>());
@@ -1595,7 +1855,8 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
   vec(s->rpart, std::max<int64_t>({s->grid_r, s->fplan.ok ? kFusedEpiMax * s->fplan.grid : 1,
                                    s->fplan2.ok ? kFusedEpiMax * s->fplan2.grid : 1}) * (kRedY + 1));
   vec(s->xpart, s->grid_s * (kRedX + 1));
-  vec(s->zpart, std::max(s->grid_z, s->grid_zt));
+  vec(s->zpart, std::max<int64_t>({s->grid_z, s->grid_zt, s->fplan.ok ? s->fplan.grid : 1,
+                                   s->fplan2.ok ? s->fplan2.grid : 1}));
   vec(s->red, 2 * s->ld + 2 * kScal + kRedX + 1);   // + CTA 0's record sums (Z step)
   if (!s->tall) {
     vec(s->ypl, m1);

@@ -24,6 +24,7 @@ CONFIGS = {
     "c4d": ("svm", 200_000, 5_000, np.float64),
     "c5d": ("tall_lasso", 200_000, 5_000, np.float64),
     "c2d": ("logistic", 100_000, 10_000, np.float64),
+    "c5": ("tall_lasso", 200_000, 5_000, np.float32),
 }
 NAMES = ["ginv_gemv_xside", "row_pass_yside", "col_pass", "slab_reduce", "y_scalars", "zstep_controller",
          "allreduce", "fused_rowcol_yside"]
