@@ -122,9 +122,18 @@ __global__ void __launch_bounds__(256) dgemm_tc_kernel(int64_t M, int64_t N, int
                                                        const double* __restrict__ A, int64_t lda, int64_t sA,
                                                        const double* __restrict__ B, int64_t ldb, int64_t sB,
                                                        double beta, double* __restrict__ C, int64_t ldc,
-                                                       int64_t sC, int lower_only) {
+                                                       int64_t sC, int lower_only, int kmode) {
   const int64_t i0 = (int64_t)blockIdx.y * TBM, j0 = (int64_t)blockIdx.x * TBN;
   if (lower_only && j0 > i0 + TBM - 1) return;
+  // Triangular operands (kmode, set by trtri / the W'W product): the K range
+  // of this tile outside which every product has a zero factor -- skipped
+  // whole TBK chunks only, so the non-zero terms are added in the same order
+  // (results identical to the full range).
+  //   1: B lower triangular (B[k][j] = 0 for k < j): k >= j0
+  //   2: A lower triangular (A[i][k] = 0 for k > i): k < i0 + TBM
+  //   3: A' with A lower triangular (A[k][i] = 0 for k < i): k >= i0
+  const int64_t kbeg = kmode == 1 ? (j0 / TBK) * TBK : (kmode == 3 ? (i0 / TBK) * TBK : 0);
+  const int64_t kend = kmode == 2 ? min(K, i0 + TBM) : K;
   A += blockIdx.z * sA;
   B += blockIdx.z * sB;
   C += blockIdx.z * sC;
@@ -173,11 +182,11 @@ __global__ void __launch_bounds__(256) dgemm_tc_kernel(int64_t M, int64_t N, int
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int fk = lane & 3, fr = lane >> 2;   // fragment k row, m/n column
-  load(0);
-  for (int64_t k0 = 0; k0 < K; k0 += TBK) {
+  if (kbeg < kend) load(kbeg);
+  for (int64_t k0 = kbeg; k0 < kend; k0 += TBK) {
     store();
     __syncthreads();
-    if (k0 + TBK < K) load(k0 + TBK);   // next slice in flight during the MMAs
+    if (k0 + TBK < kend) load(k0 + TBK);   // next slice in flight during the MMAs
 #pragma unroll
     for (int ks = 0; ks < TBK / 4; ++ks) {
       double fa[4], fb[4];
@@ -212,7 +221,7 @@ __global__ void __launch_bounds__(256) dgemm_tc_kernel(int64_t M, int64_t N, int
 template <typename TA, typename TB, bool AT, bool BT>
 static void gemm(int64_t M, int64_t N, int64_t K, double alpha, const TA* A, int64_t lda,
                  const TB* B, int64_t ldb, double beta, double* C, int64_t ldc, bool lower,
-                 cudaStream_t st, int batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0) {
+                 cudaStream_t st, int batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0, int kmode = 0) {
   if (M <= 0 || N <= 0) return;
   if constexpr (std::is_same<TA, double>::value && std::is_same<TB, double>::value) {
     static const bool simt = [] {
@@ -225,7 +234,7 @@ static void gemm(int64_t M, int64_t N, int64_t K, double alpha, const TA* A, int
     if (!simt && K >= 512) {
       dim3 grid((unsigned)ceil_div(N, TBN), (unsigned)ceil_div(M, TBM), (unsigned)batch);
       dgemm_tc_kernel<AT, BT><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC,
-                                                    lower ? 1 : 0);
+                                                    lower ? 1 : 0, kmode);
       GF_CHECK_LAUNCH();
       return;
     }
@@ -269,6 +278,7 @@ void gram_accumulate(const gf_matrix* A, bool tall, double* G, int64_t ldg, cuda
     else gemm<float, float, false, true>(q, q, A->n, 1.0, a, A->ld, a, A->ld, 0.0, G, ldg, true, st);
   } else {
     const double* a = (const double*)A->data;
+    if (tall && gram_f64_i8(A, G, ldg, st, scratch, scratch_bytes)) return;   // int8 tensor cores
     if (tall) gemm<double, double, true, false>(q, q, A->m, 1.0, a, A->ld, a, A->ld, 0.0, G, ldg, true, st);
     else gemm<double, double, false, true>(q, q, A->n, 1.0, a, A->ld, a, A->ld, 0.0, G, ldg, true, st);
   }
@@ -589,11 +599,11 @@ void trtri(double* L, int64_t q, int64_t ld, double* tmp, cudaStream_t st) {
       const double* W11 = L;                   // rows [0, s), cols [0, s)
       double* T = tmp;
       gemm<double, double, false, false>(s, s, s, 1.0, L21, ld, W11, ld, 0.0, T, ld, false, st,
-                                         (int)full, pair * ld + pair, pair * ld + pair, pair * ld + pair);
+                                         (int)full, pair * ld + pair, pair * ld + pair, pair * ld + pair, 1);
       const double* W22 = L + s * ld + s;
       double* W21 = L + s * ld;
       gemm<double, double, false, false>(s, s, s, -1.0, W22, ld, T, ld, 0.0, W21, ld, false, st,
-                                         (int)full, pair * ld + pair, pair * ld + pair, pair * ld + pair);
+                                         (int)full, pair * ld + pair, pair * ld + pair, pair * ld + pair, 2);
     }
     // ragged last pair: first half size s, second half size r2 < s
     const int64_t p0 = full * pair;
@@ -602,17 +612,17 @@ void trtri(double* L, int64_t q, int64_t ld, double* tmp, cudaStream_t st) {
       const double* L21 = L + (p0 + s) * ld + p0;
       const double* W11 = L + p0 * ld + p0;
       double* T = tmp + p0 * ld + p0;
-      gemm<double, double, false, false>(r2, s, s, 1.0, L21, ld, W11, ld, 0.0, T, ld, false, st);
+      gemm<double, double, false, false>(r2, s, s, 1.0, L21, ld, W11, ld, 0.0, T, ld, false, st, 1, 0, 0, 0, 1);
       const double* W22 = L + (p0 + s) * ld + p0 + s;
       double* W21 = L + (p0 + s) * ld + p0;
-      gemm<double, double, false, false>(r2, s, r2, -1.0, W22, ld, T, ld, 0.0, W21, ld, false, st);
+      gemm<double, double, false, false>(r2, s, r2, -1.0, W22, ld, T, ld, 0.0, W21, ld, false, st, 1, 0, 0, 0, 2);
     }
   }
 }
 
 // G^-1 = W' W from W = L^-1 (lower); lower triangle computed, then mirrored.
 void inverse_from_factor_inv(const double* W, int64_t q, int64_t ld, double* Ginv, cudaStream_t st) {
-  gemm<double, double, true, false>(q, q, q, 1.0, W, ld, W, ld, 0.0, Ginv, ld, true, st);
+  gemm<double, double, true, false>(q, q, q, 1.0, W, ld, W, ld, 0.0, Ginv, ld, true, st, 1, 0, 0, 0, 3);
   mirror_lower<<<grid2(q), dim3(32, 8), 0, st>>>(Ginv, q, ld);
   GF_CHECK_LAUNCH();
 }

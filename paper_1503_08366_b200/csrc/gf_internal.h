@@ -91,6 +91,9 @@ void gram_accumulate(const gf_matrix* A, bool tall, double* G, int64_t ldg, cuda
                      void* scratch = nullptr, size_t scratch_bytes = 0, const unsigned* amax_known = nullptr);
 void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, void* scratch = nullptr,
                  size_t scratch_bytes = 0, const unsigned* amax_known = nullptr);  // tcgen05, G += A'A
+// fp64 tall Gram on the int8 tensor cores (exact int8 slices, gf_syrk_tc.cu);
+// false when it does not apply (no scratch, GF_GRAM_F64=dmma)
+bool gram_f64_i8(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, void* scratch, size_t scratch_bytes);
 void gram_finish(double* G, int64_t q, int64_t ldg, cudaStream_t st);
 int cholesky(double* G, int64_t q, int64_t ld, int* d_info, cudaStream_t st);
 void trtri(double* L, int64_t q, int64_t ld, double* tmp, cudaStream_t st);

@@ -573,6 +573,248 @@ syrk_pre_kernel(const unsigned char* __restrict__ hi, const unsigned char* __res
   if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// ---- fp64 Gram on the int8 tensor cores -------------------------------
+// G = A'A for fp64 A (tall) without the fp64 pipe: every column c is scaled
+// by 2^-e_c (e_c: exponent of max_i |A_ic|, exact) into (-1, 1) and cut into
+// I8_S signed slices by round-to-nearest,
+//     x = q_1 2^-6 + q_2 2^-13 + ... + q_S 2^-(7S-1) + r,   q_s in [-64, 64],
+// |r| <= 2^-(7S) (every step exact in fp64; the signed remainders keep the
+// dropped terms unbiased -- truncated slices all share x's sign and bias the
+// diagonal by ~1e-13).  Products of int8 slices accumulate EXACTLY in int32
+// on the tensor cores (kind::i8), so
+//     (A'A)_jk = 2^(e_j + e_k) sum_{s+t <= S+1} 2^(2 - 7 (s+t)) (Q_s' Q_t)_jk
+// is exact up to the slicing remainder and the dropped pairs (s + t > S + 1):
+// ~2^-49 of max|A_j| max|A_k| per row and unbiased, below the rounding of an
+// fp64 dot product of 2e5 terms (the Ozaki scheme with integer slices).  One
+// int32 TMEM accumulator per anti-diagonal d = s + t (the pairs on it share
+// the weight): S accumulators of 64 columns, drained into the fp64 G every
+// I8_KCHUNK rows (int32 bound: S * 64^2 * rows < 2^31).
+//
+// Slices live in the MMA's K-major core-matrix order, slice-major:
+// byte (s, r, c) at s * slice_bytes + ((r / 16) * ncp + c) * 16 + r % 16.  A
+// 4-D tensor map (a panel's 16-byte K rows as one run, column blocks, 16-row
+// blocks, slices) moves a stage -- I8_NK 16-row blocks of every slice of the
+// 128-column A panel, and of the 64-column B panel -- in ONE copy each,
+// straight into the layout the descriptors read (A: K-block stride 2 KB,
+// B: 1 KB; 8-row groups 128 B apart).  Warp roles as in syrk_pre_kernel:
+// epilogue 0-3, MMA 4, loader 5.
+constexpr int I8_S = 7;                        // slices (7 bits each)
+constexpr int I8_TN = 64;                      // tile columns: I8_S x 64 TMEM columns <= 512
+constexpr int I8_NK = 4;                       // 16-row K blocks per stage (2 MMAs of K = 32)
+constexpr int I8_NST = 2;                      // stages
+constexpr int I8_KCHUNK = 32768;               // rows per int32 accumulation
+constexpr int I8_A_SLICE = I8_NK * TM * 16;    // 8 KB
+constexpr int I8_B_SLICE = I8_NK * I8_TN * 16; // 4 KB
+constexpr int I8_A_STAGE = I8_S * I8_A_SLICE;  // 56 KB
+constexpr int I8_STAGE = I8_S * (I8_A_SLICE + I8_B_SLICE);   // 84 KB
+constexpr int I8_SMEM = I8_NST * I8_STAGE;     // 168 KB
+constexpr int I8_THREADS = 6 * 32;
+// D s32 (2), A/B signed int8 (1), K-major, N = 64, M = 128
+constexpr uint32_t I8_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(I8_TN >> 3) << 17) |
+                              ((uint32_t)(TM >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(I8_IDESC), "r"(accumulate));
+}
+
+// per-column max |A| as fp64 bits (non-negative doubles order like their bits)
+__global__ void colmax_f64_kernel(const double* __restrict__ A, int64_t m, int64_t ld, int64_t n,
+                                  unsigned long long* __restrict__ cmax) {
+  const int64_t rows_per = (m + gridDim.y - 1) / gridDim.y;
+  const int64_t r0 = blockIdx.y * rows_per, r1 = min(m, r0 + rows_per);
+  for (int64_t c = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+    double mx = 0.0;
+    for (int64_t r = r0; r < r1; ++r) mx = fmax(mx, fabs(A[r * ld + c]));
+    if (mx > 0.0) atomicMax(cmax + c, (unsigned long long)__double_as_longlong(mx));
+  }
+}
+
+// slices of the 16-row block kb, column c (one thread each): 16 doubles in,
+// I8_S x 16 int8 out (one 16-byte store per slice)
+__global__ void __launch_bounds__(256) slice_i8_kernel(const double* __restrict__ A, int64_t m, int64_t ld, int64_t n,
+                                                       int64_t ncp, int64_t nkb,
+                                                       const unsigned long long* __restrict__ cmax,
+                                                       uint4* __restrict__ Q, int64_t slice_vecs) {
+  for (int64_t idx = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; idx < nkb * ncp;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t kb = idx / ncp, c = idx - kb * ncp;
+    int e = 0;
+    if (c < n) {
+      const double mx = __longlong_as_double((long long)cmax[c]);
+      if (mx > 0.0) frexp(mx, &e);   // mx in [2^(e-1), 2^e)
+    }
+    double r[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int64_t row = kb * 16 + t;
+      r[t] = (row < m && c < n) ? ldexp(A[row * ld + c], 6 - e) : 0.0;   // (-64, 64)
+    }
+#pragma unroll
+    for (int sl = 0; sl < I8_S; ++sl) {
+      uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const double qd = rint(r[t]);             // |qd| <= 64
+        r[t] = (r[t] - qd) * 128.0;               // exact, [-64, 64]
+        w[t >> 2] |= ((uint32_t)(int)qd & 0xffu) << (8 * (t & 3));
+      }
+      Q[sl * slice_vecs + idx] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+__global__ void colexp_kernel(const unsigned long long* __restrict__ cmax, int64_t n, int* __restrict__ ex) {
+  for (int64_t c = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+    int e = 0;
+    const double mx = __longlong_as_double((long long)cmax[c]);
+    if (mx > 0.0) frexp(mx, &e);
+    ex[c] = e;
+  }
+}
+
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(I8_THREADS, 1)
+syrk_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t nkb,
+               int64_t q, const int2* __restrict__ tiles, const int* __restrict__ ex, double* __restrict__ G,
+               int64_t ldg) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[I8_NST], empty[I8_NST], accf, acce;
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int2 tile = tiles[blockIdx.x];
+  const int64_t i0 = (int64_t)tile.x * TM, j0 = (int64_t)tile.y * I8_TN;
+  const int64_t nstages = nkb / I8_NK;
+  const int64_t SPC = I8_KCHUNK / (16 * I8_NK);
+  const int64_t nchunks = (nstages + SPC - 1) / SPC;
+
+  if (tid == 0) {
+    for (int s = 0; s < I8_NST; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], 1);
+    }
+    bar_init(&accf, 1);
+    bar_init(&acce, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base_s)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 5) {
+    // ===================== loader: two tensor copies per stage =====================
+    if (lane == 0) {
+      for (int64_t it = 0; it < nstages; ++it) {
+        const int s = (int)(it % I8_NST);
+        if (it >= I8_NST) bar_wait(&empty[s], (unsigned)(((it / I8_NST) - 1) & 1));
+        const uint32_t st = su32(smem + (size_t)s * I8_STAGE), bar = su32(&full[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)I8_STAGE)
+                     : "memory");
+        const int kb = (int)(it * I8_NK);
+        tma_load_4d(st, &tmA, 0, (int)(i0 / TM), kb, 0, bar);
+        tma_load_4d(st + I8_A_STAGE, &tmB, 0, (int)(j0 / I8_TN), kb, 0, bar);
+      }
+    }
+  } else if (warp == 4) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      constexpr uint32_t LBO_A = TM * 16, LBO_B = I8_TN * 16;
+      for (int64_t c = 0; c < nchunks; ++c) {
+        if (c >= 1) bar_wait(&acce, (unsigned)((c - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int64_t it0 = c * SPC, it1 = min(nstages, it0 + SPC);
+        for (int64_t it = it0; it < it1; ++it) {
+          const int s = (int)(it % I8_NST);
+          bar_wait(&full[s], (unsigned)((it / I8_NST) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = su32(smem + (size_t)s * I8_STAGE), sb = sa + I8_A_STAGE;
+#pragma unroll
+          for (int kk = 0; kk < I8_NK / 2; ++kk) {
+#pragma unroll
+            for (int ps = 0; ps < I8_S; ++ps)
+#pragma unroll
+              for (int pt = 0; pt + ps < I8_S; ++pt) {   // s + t <= S + 1 with 1-based slices
+                const uint64_t da = smem_desc(sa + ps * I8_A_SLICE + 2 * kk * LBO_A, LBO_A, 128);
+                const uint64_t db = smem_desc(sb + pt * I8_B_SLICE + 2 * kk * LBO_B, LBO_B, 128);
+                const int d = ps + pt;                   // anti-diagonal: accumulator d
+                // the first product into each accumulator of a chunk overwrites it
+                mma_i8(tmem + (uint32_t)(d * I8_TN), da, db, (it > it0 || kk > 0 || ps > 0) ? 1u : 0u);
+              }
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&accf);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== epilogue (warps 0-3): drain into fp64 G =====================
+    const int64_t i = i0 + warp * 32 + lane;
+    const int ei = i < q ? ex[i] : 0;
+    for (int64_t c = 0; c < nchunks; ++c) {
+      bar_wait(&accf, (unsigned)(c & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+      for (int cc = 0; cc < I8_TN / 16; ++cc) {
+        uint32_t v[I8_S][16];
+#pragma unroll
+        for (int d = 0; d < I8_S; ++d) {
+          const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(d * I8_TN + cc * 16);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+              "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[d][0]), "=r"(v[d][1]), "=r"(v[d][2]), "=r"(v[d][3]), "=r"(v[d][4]), "=r"(v[d][5]),
+                "=r"(v[d][6]), "=r"(v[d][7]), "=r"(v[d][8]), "=r"(v[d][9]), "=r"(v[d][10]), "=r"(v[d][11]),
+                "=r"(v[d][12]), "=r"(v[d][13]), "=r"(v[d][14]), "=r"(v[d][15])
+              : "r"(taddr));
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (i < q) {
+          const int64_t jb = j0 + cc * 16;
+          const int64_t jn = min((int64_t)16, q - jb);
+          double* col = G + jb * ldg + i;
+          double g[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t) g[t] = t < jn ? col[t * ldg] : 0.0;
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            if (t >= jn) continue;
+            // Horner from the least significant anti-diagonal: sum_d 2^(-7 d - 12) acc_d
+            double sum = (double)(int)v[I8_S - 1][t];
+#pragma unroll
+            for (int d = I8_S - 2; d >= 0; --d) sum = fma(sum, 0x1p-7, (double)(int)v[d][t]);
+            col[t * ldg] = g[t] + ldexp(sum, ei + ex[jb + t] - 12);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) bar_arrive(&acce);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // The kernel accumulates the upper triangle (transposed tile writes); copy it
 // down so callers see the usual lower-triangle result.
 __global__ void upper_to_lower(double* G, int64_t q, int64_t ld) {
@@ -607,7 +849,17 @@ static CUtensorMap panel_map(const gf_matrix* A, int box_cols) {
   return m;
 }
 
+static bool gram_i8_enabled() {
+  const char* e = getenv("GF_GRAM_F64");   // "dmma": the fp64 tensor-core GEMM instead of the int8 slices
+  return !(e && std::string(e) == "dmma");
+}
+
+static int64_t i8_ncp(int64_t q) { return ceil_div(q, syrk::TM) * syrk::TM; }
+static int64_t i8_nkb(int64_t m) { return ceil_div(m, 16 * syrk::I8_NK) * syrk::I8_NK; }
+
 size_t gram_scratch_bytes(const gf_matrix* A, bool tall) {
+  if (tall && A->dtype == GF_F64)
+    return gram_i8_enabled() ? (size_t)syrk::I8_S * i8_nkb(A->m) * i8_ncp(A->n) * 16 : 0;
   const char* sp = getenv("GF_SYRK");   // "tf32" / "f16": the in-kernel converters, no copy
   if (!tall || A->dtype != GF_F32 || (sp && (std::string(sp) == "tf32" || std::string(sp) == "f16"))) return 0;
   const int64_t ncp = ceil_div(A->n, syrk::TN) * syrk::TN, nkb = ceil_div(A->m, syrk::BK * syrk::PRE_SUB) * 2 * syrk::PRE_SUB;
@@ -749,6 +1001,89 @@ void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, vo
   upper_to_lower<<<dim3((unsigned)ceil_div(q, 32), (unsigned)ceil_div(q, 8)), dim3(32, 8), 0, st>>>(G, q, ldg);
   GF_CHECK_LAUNCH();
   GF_CUDA(cudaStreamSynchronize(st));
+}
+
+// fp64 tall Gram on the int8 tensor cores (see syrk_i8_kernel); `scratch`
+// holds the slices (gram_scratch_bytes).  G (zeroed by the caller) += A'A.
+bool gram_f64_i8(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, void* scratch, size_t scratch_bytes) {
+  using namespace syrk;
+  const int64_t m = A->m, q = A->n;
+  const int64_t ncp = i8_ncp(q), nkb = i8_nkb(m);
+  const size_t slice_bytes = (size_t)nkb * ncp * 16;
+  if (!gram_i8_enabled() || scratch == nullptr || scratch_bytes < (size_t)I8_S * slice_bytes || m <= 0 || q <= 0)
+    return false;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult qr;
+    void* fn = nullptr;
+    GF_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+    GF_REQUIRE(fn != nullptr && qr == cudaDriverEntryPointSuccess, GF_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  // 8-byte words: (the 16-byte K rows of a panel's columns -- one contiguous
+  // run per 16-row block: 2 KB for the 128 A columns, 1 KB for the 64 B
+  // columns --, column blocks, 16-row blocks, slices).  Long inner runs: a
+  // 16-byte inner box dimension ran the copy engine at ~16 B per cycle.
+  CUtensorMap tmA, tmB;
+  for (int w = 0; w < 2; ++w) {
+    const int64_t cols = w == 0 ? TM : I8_TN;
+    const cuuint64_t dims[4] = {(cuuint64_t)(cols * 2), (cuuint64_t)(ncp / cols), (cuuint64_t)nkb, (cuuint64_t)I8_S};
+    const cuuint64_t strides[3] = {(cuuint64_t)cols * 16, (cuuint64_t)ncp * 16, (cuuint64_t)slice_bytes};
+    const cuuint32_t box[4] = {(cuuint32_t)(cols * 2), 1, (cuuint32_t)I8_NK, (cuuint32_t)I8_S};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = encode(w == 0 ? &tmA : &tmB, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, scratch, dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    GF_REQUIRE(r == CUDA_SUCCESS, GF_E_CUDA, "cuTensorMapEncodeTiled (int8 slices) failed");
+  }
+  std::vector<int2> tl;   // tiles (I: 128 rows of A'A, J: 64 columns) with j0 < i0 + 128: covers j <= i
+  for (int64_t bi = 0; bi < ceil_div(q, TM); ++bi)
+    for (int64_t bj = 0; bj * I8_TN < std::min((bi + 1) * TM, q); ++bj) tl.push_back(make_int2((int)bi, (int)bj));
+  DBuf small(tl.size() * sizeof(int2) + (size_t)q * (sizeof(unsigned long long) + sizeof(int)) + 64);
+  int2* d_tiles = small.as<int2>();
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(small.as<char>() + ((tl.size() * sizeof(int2) + 15) / 16) * 16);
+  int* ex = reinterpret_cast<int*>(cmax + q);
+  GF_CUDA(cudaMemcpyAsync(d_tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+  GF_CUDA(cudaMemsetAsync(cmax, 0, q * sizeof(unsigned long long), st));
+  const char* vb = getenv("GF_VERBOSE_SETUP");
+  const bool verbose = vb && vb[0] == '1';
+  cudaEvent_t ev[3];
+  if (verbose) {
+    for (auto& e : ev) GF_CUDA(cudaEventCreate(&e));
+    GF_CUDA(cudaEventRecord(ev[0], st));
+  }
+  {
+    const unsigned gx = (unsigned)ceil_div(q, 256);
+    const unsigned gy = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div((int64_t)num_sms() * 8, gx), m));
+    colmax_f64_kernel<<<dim3(gx, gy), 256, 0, st>>>((const double*)A->data, m, A->ld, q, cmax);
+    GF_CHECK_LAUNCH();
+    colexp_kernel<<<(unsigned)ceil_div(q, 256), 256, 0, st>>>(cmax, q, ex);
+    GF_CHECK_LAUNCH();
+    slice_i8_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nkb * ncp, 256), num_sms() * 16), 256, 0, st>>>(
+        (const double*)A->data, m, A->ld, q, ncp, nkb, cmax, (uint4*)scratch, (int64_t)(slice_bytes / 16));
+    GF_CHECK_LAUNCH();
+  }
+  if (verbose) GF_CUDA(cudaEventRecord(ev[1], st));
+  static bool attr = false;
+  if (!attr) {
+    GF_CUDA(cudaFuncSetAttribute(syrk_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, I8_SMEM));
+    attr = true;
+  }
+  syrk_i8_kernel<<<(unsigned)tl.size(), I8_THREADS, I8_SMEM, st>>>(tmA, tmB, nkb, q, d_tiles, ex, G, ldg);
+  GF_CHECK_LAUNCH();
+  upper_to_lower<<<dim3((unsigned)ceil_div(q, 32), (unsigned)ceil_div(q, 8)), dim3(32, 8), 0, st>>>(G, q, ldg);
+  GF_CHECK_LAUNCH();
+  if (verbose) {
+    GF_CUDA(cudaEventRecord(ev[2], st));
+    GF_CUDA(cudaStreamSynchronize(st));
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    fprintf(stderr, "[gf] gram fp64 int8 slices: slice %.2f ms, syrk %.2f ms (%zu tiles)\n", a, b, tl.size());
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+  GF_CUDA(cudaStreamSynchronize(st));   // `small` is freed on return
+  return true;
 }
 
 }  // namespace gf

@@ -315,6 +315,40 @@ def test_gram_f16_split_scaling(scale):
     assert err.max() < 2e-5, err.max()
 
 
+@pytest.mark.parametrize("shape", [(17, 17), (300, 257), (513, 129), (3000, 700), (20000, 1300), (70000, 300)])
+def test_gram_int8_slices_fp64(shape):
+    """The fp64 Gram runs on the int8 tensor cores (tcgen05 kind::i8, seven
+    exact 7-bit slices per column, int32 accumulation drained to fp64 every
+    8192 rows): it must match an fp64 Gram to fp64-dot-product accuracy,
+    relative to sqrt(G_ii G_jj), across ragged tiles, several drains
+    (70000 rows) and columns spanning twelve orders of magnitude."""
+    m, n = shape
+    rng = np.random.default_rng(m * 7 + n)
+    A = rng.normal(size=(m, n)) * np.logspace(-6, 6, n)[None, :]
+    A[:, n // 3] = 0.0                         # an all-zero column (exponent 0)
+    G = gf.build_projector(A).gram
+    ref = A.T @ A
+    d = np.sqrt(np.maximum(np.diag(ref), 1e-300))
+    off = ~np.eye(n, dtype=bool)
+    err = (np.abs(G - ref) / np.outer(d, d))[off]
+    assert np.isfinite(G).all()
+    assert err.max() < 1e-13, err.max()
+    # the diagonal carries the added identity: its absolute resolution is ~eps
+    dg = np.abs(np.diag(G) - 1.0 - np.diag(ref)) / np.maximum(np.diag(ref), 1.0)
+    assert dg.max() < 1e-13
+    np.testing.assert_allclose(G, G.T, rtol=0, atol=0)
+
+
+def test_gram_int8_matches_dmma_path(monkeypatch):
+    """The same Gram through the fp64 DMMA GEMM (GF_GRAM_F64=dmma)."""
+    A = np.random.default_rng(3).normal(size=(5000, 700))
+    G8 = gf.build_projector(A).gram
+    monkeypatch.setenv("GF_GRAM_F64", "dmma")
+    Gd = gf.build_projector(A).gram
+    scale = np.sqrt(np.outer(np.diag(Gd), np.diag(Gd)))
+    assert (np.abs(G8 - Gd) / scale).max() < 1e-13
+
+
 CONJ = _cases.load("conj")
 
 
