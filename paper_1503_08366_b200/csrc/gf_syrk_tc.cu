@@ -576,19 +576,21 @@ syrk_pre_kernel(const unsigned char* __restrict__ hi, const unsigned char* __res
 // ---- fp64 Gram on the int8 tensor cores -------------------------------
 // G = A'A for fp64 A (tall) without the fp64 pipe: every column c is scaled
 // by 2^-e_c (e_c: exponent of max_i |A_ic|, exact) into (-1, 1) and cut into
-// I8_S signed slices by round-to-nearest,
-//     x = q_1 2^-6 + q_2 2^-13 + ... + q_S 2^-(7S-1) + r,   q_s in [-64, 64],
-// |r| <= 2^-(7S) (every step exact in fp64; the signed remainders keep the
-// dropped terms unbiased -- truncated slices all share x's sign and bias the
-// diagonal by ~1e-13).  Products of int8 slices accumulate EXACTLY in int32
-// on the tensor cores (kind::i8), so
+// I8_S = 8 signed slices by round-to-nearest,
+//     x = q_1 2^-6 + q_2 2^-13 + ... + q_8 2^-55 + r,   q_s in [-64, 64],
+// |r| <= 2^-56 (every step exact in fp64; the signed remainders keep the
+// dropped terms unbiased -- truncated slices all share x's sign and biased
+// the diagonal by ~1e-13).  Products of int8 slices accumulate EXACTLY in
+// int32 on the tensor cores (kind::i8), so
 //     (A'A)_jk = 2^(e_j + e_k) sum_{s+t <= S+1} 2^(2 - 7 (s+t)) (Q_s' Q_t)_jk
-// is exact up to the slicing remainder and the dropped pairs (s + t > S + 1):
-// ~2^-49 of max|A_j| max|A_k| per row and unbiased, below the rounding of an
-// fp64 dot product of 2e5 terms (the Ozaki scheme with integer slices).  One
-// int32 TMEM accumulator per anti-diagonal d = s + t (the pairs on it share
-// the weight): S accumulators of 64 columns, drained into the fp64 G every
-// I8_KCHUNK rows (int32 bound: S * 64^2 * rows < 2^31).
+// is exact up to the slicing remainder and the dropped pairs s + t >= S + 2
+// (~2^-56 of max|A_j| max|A_k| per row, unbiased): at or below the rounding
+// of an fp64 dot product (the Ozaki scheme with integer slices; the error is
+// "fixed point" relative to the column maxima -- seven slices left ~1e-14
+// absolute on O(1) entries).  One int32 TMEM accumulator per anti-diagonal
+// d = s + t (the pairs on it share the weight): S accumulators of 64
+// columns = all 512 TMEM columns, drained into the fp64 G every I8_KCHUNK
+// rows (int32 bound: S * 64^2 * rows < 2^31).
 //
 // Slices live in the MMA's K-major core-matrix order, slice-major:
 // byte (s, r, c) at s * slice_bytes + ((r / 16) * ncp + c) * 16 + r % 16.  A
@@ -598,16 +600,16 @@ syrk_pre_kernel(const unsigned char* __restrict__ hi, const unsigned char* __res
 // straight into the layout the descriptors read (A: K-block stride 2 KB,
 // B: 1 KB; 8-row groups 128 B apart).  Warp roles as in syrk_pre_kernel:
 // epilogue 0-3, MMA 4, loader 5.
-constexpr int I8_S = 7;                        // slices (7 bits each)
+constexpr int I8_S = 8;                        // slices (7 bits each; anti-diagonals kept: S)
 constexpr int I8_TN = 64;                      // tile columns: I8_S x 64 TMEM columns <= 512
 constexpr int I8_NK = 4;                       // 16-row K blocks per stage (2 MMAs of K = 32)
 constexpr int I8_NST = 2;                      // stages
 constexpr int I8_KCHUNK = 32768;               // rows per int32 accumulation
 constexpr int I8_A_SLICE = I8_NK * TM * 16;    // 8 KB
 constexpr int I8_B_SLICE = I8_NK * I8_TN * 16; // 4 KB
-constexpr int I8_A_STAGE = I8_S * I8_A_SLICE;  // 56 KB
-constexpr int I8_STAGE = I8_S * (I8_A_SLICE + I8_B_SLICE);   // 84 KB
-constexpr int I8_SMEM = I8_NST * I8_STAGE;     // 168 KB
+constexpr int I8_A_STAGE = I8_S * I8_A_SLICE;  // 64 KB
+constexpr int I8_STAGE = I8_S * (I8_A_SLICE + I8_B_SLICE);   // 96 KB
+constexpr int I8_SMEM = I8_NST * I8_STAGE;     // 192 KB
 constexpr int I8_THREADS = 6 * 32;
 // D s32 (2), A/B signed int8 (1), K-major, N = 64, M = 128
 constexpr uint32_t I8_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(I8_TN >> 3) << 17) |

@@ -10,7 +10,8 @@ path = sys.argv[1]
 rows = [r for r in csv.reader(open(path)) if len(r) == 15 and r[0] != "ID"]
 launches = [(re.sub(r"\(.*", "", r[4]).replace("void ", ""), float(r[14]) / 1e3) for r in rows]
 names = [n for n, _ in launches]
-first = next(i for i, n in enumerate(names) if "fused_rowcol" in n or "rowgemv" in n)
+first = next(i for i, n in enumerate(names)
+             if "fused_rowcol" in n or re.search(r"rowgemv_kernel<\w+, 2", n))
 # the setup preceding the first iteration: walk back to the first equilibration launch of that prepare
 setup_start = max(i for i, n in enumerate(names[:first]) if "sq_row" in n or "equil" in n.lower()) if first else 0
 while setup_start > 0 and ("sq_row" in names[setup_start - 1] or "col_update" in names[setup_start - 1]
