@@ -647,22 +647,27 @@ __device__ __forceinline__ void st_async_f64(uint32_t cluster_addr, double v, ui
 }
 
 struct FusedPlan2 {
+  int cl = 0;          // CTAs per cluster (2, 4 or 8): each streams 1/cl of every row
   int cw = 0, ne = 0, nv = 0, nslot = 0, tr = 0;
-  int grid = 0;        // CTAs (2 per cluster)
-  int64_t hvec = 0;    // 16-byte vectors of a row in CTA 0's half (CTA 1: nvec - hvec)
+  int grid = 0;        // CTAs (cl per cluster)
+  int64_t hvec = 0;    // 16-byte vectors of the widest share of a row (the slot size)
   size_t smem = 0;
   bool ok = false;
 };
 
-// max_clusters: co-resident 2-CTA clusters at this shared-memory size
+// share of a row that CTA `rank` of a cl-CTA cluster streams: 16-byte vectors [v0, v1)
+__host__ __device__ inline int64_t cl_vec_begin(int64_t nvec, int rank, int cl) { return nvec * rank / cl; }
+
+// max_clusters: co-resident cl-CTA clusters at this shared-memory size
 // (cudaOccupancyMaxActiveClusters): the kernel is persistent, every cluster
 // must be resident in one wave.
-inline FusedPlan2 plan_fused_cl2(int64_t m, int64_t ld, int esize, int sms, size_t smem_max, int max_clusters,
-                                 int max_slots = kMaxSlots) {
+inline FusedPlan2 plan_fused_cl(int64_t m, int64_t ld, int esize, int sms, size_t smem_max, int max_clusters, int cl,
+                                int max_slots = kMaxSlots) {
   FusedPlan2 p;
+  p.cl = cl;
   const int vn = 16 / esize;
   const int64_t nvec = ld / vn;
-  p.hvec = (nvec + 1) / 2;
+  p.hvec = ceil_div(nvec, (int64_t)cl);
   p.cw = 20;
   for (int cw : {8, 12, 16, 20})
     if (ceil_div(p.hvec, cw * 32) <= (cw <= 12 ? 5 : 4)) { p.cw = cw; break; }
@@ -673,20 +678,27 @@ inline FusedPlan2 plan_fused_cl2(int64_t m, int64_t ld, int esize, int sms, size
   p.nslot = (int)std::min<size_t>(std::min(max_slots, kMaxSlots), budget / slot_bytes);
   const int want_pf = std::max<int>(2, (int)ceil_div(48 * 1024, (int64_t)slot_bytes));
   p.tr = 0;
-  for (int tr : {4, 2, 1})
-    if (3 * tr + want_pf <= p.nslot || (tr == 1 && 3 + 1 <= p.nslot)) { p.tr = tr; break; }
-  const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms / 2, (int64_t)max_clusters, m}));
-  p.grid = (int)(2 * ncl);
+  for (int tr : {4, 2, 1})   // (2 TR (cl - 1) partials per group go out on distinct lanes)
+    if ((3 * tr + want_pf <= p.nslot || (tr == 1 && 3 + 1 <= p.nslot)) && 2 * tr * (cl - 1) <= 32) {
+      p.tr = tr;
+      break;
+    }
+  const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms / cl, (int64_t)max_clusters, m}));
+  p.grid = (int)(cl * ncl);
   p.smem = (size_t)p.nslot * slot_bytes;
-  p.ok = max_clusters >= 1 && p.hvec >= 1 && nvec - p.hvec >= 1 && p.nv >= 1 && p.nv <= 6 && p.tr >= 1 && m > 0;
+  // every CTA needs a non-empty share
+  const bool shares = nvec >= cl && cl_vec_begin(nvec, 1, cl) >= 1;
+  p.ok = max_clusters >= 1 && shares && p.nv >= 1 && p.nv <= 6 && p.tr >= 1 && m > 0 &&
+         (cl == 2 || p.cw == 8);   // (the 4- and 8-CTA instances exist for 8 compute warps)
   return p;
 }
 
-template <typename T, int NV, int TR, int CW, class Epi, class Tail = NoTail>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fused_threads(CW), 1)
-fused_rowcol_cl2_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* __restrict__ x0,
-                        const T* __restrict__ x1, Epi epi, int nslot, int64_t hvec, double* __restrict__ rpart,
-                        double* __restrict__ cpart, Tail tail = Tail{}) {
+// CL CTAs per cluster (2, 4, 8; the cluster shape is a launch attribute).
+template <typename T, int NV, int TR, int CW, int CL, class Epi, class Tail = NoTail>
+__global__ void __launch_bounds__(fused_threads(CW), 1)
+fused_rowcol_cl_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* __restrict__ x0,
+                       const T* __restrict__ x1, Epi epi, int nslot, int64_t hvec, double* __restrict__ rpart,
+                       double* __restrict__ cpart, Tail tail = Tail{}) {
   using V = typename Vec16<T>::type;
   constexpr int VN = Vec16<T>::n;
   constexpr int NR = Epi::NR;
@@ -700,17 +712,19 @@ fused_rowcol_cl2_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const
   static_assert(CW <= 32, "one epilogue lane per compute warp");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxSlots], sfree[kMaxSlots];
+  static_assert(CL == 2 || CL == 4 || CL == 8, "cluster of 2, 4 or 8 CTAs");
+  static_assert(K * (CL - 1) <= 32, "one lane per (value, peer) partial");
   __shared__ __align__(8) uint64_t redf[NE], rede[NE], wf[NE], we[NE], xf[NE][2];
   __shared__ T red_s[NE][kFusedWarps][K];
   __shared__ __align__(8) T w_s[NE][TR][2];
-  __shared__ __align__(8) double xbuf[NE][2][K];
+  __shared__ __align__(8) double xbuf[NE][2][CL][K];   // [buffer][use parity][source rank][value]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t rank = cluster_ctarank(), peer = rank ^ 1u;
-  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const uint32_t rank = cluster_ctarank();
+  const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   const int64_t nvec_all = ld / VN;
-  const int64_t v0 = rank ? hvec : 0;                      // first 16-byte vector of this CTA's half
-  const int64_t nvec = rank ? nvec_all - hvec : hvec;      // vectors of this CTA's half
+  const int64_t v0 = cl_vec_begin(nvec_all, (int)rank, CL);      // first 16-byte vector of this CTA's share
+  const int64_t nvec = cl_vec_begin(nvec_all, (int)rank + 1, CL) - v0;
   const unsigned sb = (unsigned)(hvec * 16);               // slot stride
   const unsigned cb = (unsigned)(nvec * 16);               // bytes copied per row
   const int64_t r0 = rows * cid / ncl;
@@ -771,15 +785,22 @@ fused_rowcol_cl2_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const
 #pragma unroll
       for (int k = 0; k < (NR > 0 ? NR : 1); ++k) ered[k] = 0.0;
       unsigned eflags = 0;
-      const uint32_t xb_peer = mapa_u32(smem_u32(&xbuf[b][0][0]), peer);
-      const uint32_t xf_peer = mapa_u32(smem_u32(&xf[b][0]), peer);
+      // lane l < K (CL - 1) sends value l % K to peer (rank + 1 + l / K) % CL
+      const int sq = lane % K;
+      const uint32_t speer = (rank + 1u + (uint32_t)(lane / K)) % (uint32_t)CL;
+      const bool sender = lane < K * (CL - 1);
+      const uint32_t xb_peer = mapa_u32(smem_u32(&xbuf[b][0][rank][sq]), speer);   // my slot in the peer's buffer
+      const uint32_t xf_peer = mapa_u32(smem_u32(&xf[b][0]), speer);
       const uint32_t xf_loc = smem_u32(&xf[b][0]), we_loc = smem_u32(&we[b]), redf_loc = smem_u32(&redf[b]);
+      constexpr uint32_t kUseStride = (uint32_t)(CL * K * sizeof(double));   // xbuf[b][1] - xbuf[b][0]
       typename Epi::RowIn in{};
       if (lane < TR && par * TR + lane < nr) in = epi.load_in(r0 + par * TR + lane);
       for (int ge = par; ge < ng; ge += NE) {
         const unsigned use = (unsigned)(ge / NE), p = use & 1u;
         mbar_wait_u32(redf_loc, use & 1u);
-        constexpr int RW = CW <= 16 ? 16 : 32;
+        // the sending lanes (< K (CL - 1)) must all hold the totals: a
+        // half-warp butterfly leaves lanes 16-31 with their own (zero) half
+        constexpr int RW = (CW <= 16 && K * (CL - 1) <= 16) ? 16 : 32;
         double v[K];
 #pragma unroll
         for (int q = 0; q < K; ++q) v[q] = lane < kFusedWarps ? (double)red_s[b][lane][q] : 0.0;
@@ -789,24 +810,33 @@ fused_rowcol_cl2_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const
         for (int q = 0; q < K; ++q)
 #pragma unroll
           for (int o = RW / 2; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o, RW);
-        // this CTA's partials -> the peer's xbuf[b][p] (lane q sends value q)
+        // this CTA's partials -> slot [rank] of every peer's xbuf[b][p]
+        double mine_q = v[0];
 #pragma unroll
-        for (int q = 0; q < K; ++q)
-          if (lane == q) st_async_f64(xb_peer + 8u * (unsigned)(p * K + q), v[q], xf_peer + 8u * p);
-        if (lane == 0) mbar_arrive_expect_tx(&xf[b][p], (unsigned)(K * sizeof(double)));
-        mbar_wait_u32(xf_loc + 8u * p, (use >> 1) & 1u);   // the peer's partials have landed
+        for (int q = 1; q < K; ++q)
+          if (sq == q) mine_q = v[q];
+        if (sender) st_async_f64(xb_peer + p * kUseStride, mine_q, xf_peer + 8u * p);
+        if (lane == 0) mbar_arrive_expect_tx(&xf[b][p], (unsigned)((CL - 1) * K * sizeof(double)));
+        mbar_wait_u32(xf_loc + 8u * p, (use >> 1) & 1u);   // every peer's partials have landed
         const int g = min(TR, nr - ge * TR);
         double dots[2] = {0.0, 0.0};
 #pragma unroll
         for (int rr = 0; rr < TR; ++rr)
-          if (rr == lane) {
-            const double p0 = xbuf[b][p][2 * rr], p1 = xbuf[b][p][2 * rr + 1];
-            dots[0] = rank == 0 ? v[2 * rr] + p0 : p0 + v[2 * rr];
-            dots[1] = rank == 0 ? v[2 * rr + 1] + p1 : p1 + v[2 * rr + 1];
+          if (rr == lane) {   // rank order 0 .. CL-1 (this CTA's own partial in its place): the same sum everywhere
+            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int r = 0; r < CL; ++r) {
+              const double p0 = r == (int)rank ? v[2 * rr] : xbuf[b][p][r][2 * rr];
+              const double p1 = r == (int)rank ? v[2 * rr + 1] : xbuf[b][p][r][2 * rr + 1];
+              d0 = r == 0 ? p0 : d0 + p0;
+              d1 = r == 0 ? p1 : d1 + p1;
+            }
+            dots[0] = d0;
+            dots[1] = d1;
           }
-        // every row's weights are computed here (mid is pure: both CTAs get
-        // the same values); tail() only for this CTA's rows
-        const bool mine = lane < g && (((ge * TR + lane) & 1) == (int)rank);
+        // every row's weights are computed here (mid is pure: every CTA gets
+        // the same values); tail() only for this CTA's rows (row j: CTA j mod CL)
+        const bool mine = lane < g && ((ge * TR + lane) % CL == (int)rank);
         typename Epi::Mid md{};
         double w0 = 0.0, w1 = 0.0;
         if (lane < g) md = epi.mid(in, dots, w0, w1);

@@ -1365,52 +1365,84 @@ static void fused_dispatch(gf_solver* s, cudaStream_t st, bool attr_only) {
 
 // Two-CTA cluster variant.  attr_only: set the shared-memory limit and
 // return the number of co-resident clusters of this instance.
-template <typename T, int NV, int TR, int CW>
+template <typename T, int NV, int TR, int CW, int CL>
 static int fused2_go(gf_solver* s, cudaStream_t st, bool attr_only) {
   const FusedPlan2& p = s->fplan2;
-  auto kern = fused_rowcol_cl2_kernel<T, NV, TR, CW, YEpi<T>, ZTail<T>>;
+  auto kern = fused_rowcol_cl_kernel<T, NV, TR, CW, CL, YEpi<T>, ZTail<T>>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(attr_only ? CL * (num_sms() / CL) : p.grid));
+  cfg.blockDim = dim3(fused_threads(CW));
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
   if (attr_only) {
     GF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * (num_sms() / 2)));
-    cfg.blockDim = dim3(fused_threads(CW));
-    cfg.dynamicSmemBytes = p.smem;
+    if (CL > 8) GF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cfg.numAttrs = 1;
     int ncl = 0;
     GF_CUDA(cudaOccupancyMaxActiveClusters(&ncl, (void*)kern, &cfg));
     return ncl;
   }
-  launch_k(use_pdl(s), kern, dim3(p.grid), dim3(fused_threads(CW)), p.smem, st, (const T*)s->S->A->data, s->m,
-           s->ld, (const T*)s->xk_T.as<T>(), (const T*)s->xh_T.as<T>(), make_yepi<T>(s), p.nslot, p.hvec,
-           s->rpart.as<double>(), s->cpart.as<double>(), make_ztail<T>(s, p.grid / 2, (int64_t)p.ne * p.grid));
+  cfg.numAttrs = use_pdl(s) ? 2 : 1;
+  GF_CUDA(cudaLaunchKernelEx(&cfg, kern, (const T*)s->S->A->data, s->m, s->ld, (const T*)s->xk_T.as<T>(),
+                             (const T*)s->xh_T.as<T>(), make_yepi<T>(s), p.nslot, p.hvec, s->rpart.as<double>(),
+                             s->cpart.as<double>(), make_ztail<T>(s, p.grid / CL, (int64_t)p.ne * p.grid)));
   GF_CHECK_LAUNCH();
   return 0;
 }
 
-template <typename T, int NV, int CW>
+template <typename T, int NV, int CW, int CL>
 static int fused2_tr(gf_solver* s, cudaStream_t st, bool attr_only) {
-  return s->fplan2.tr >= 2 ? fused2_go<T, NV, 2, CW>(s, st, attr_only) : fused2_go<T, NV, 1, CW>(s, st, attr_only);
+  return s->fplan2.tr >= 2 ? fused2_go<T, NV, 2, CW, CL>(s, st, attr_only) : fused2_go<T, NV, 1, CW, CL>(s, st, attr_only);
+}
+
+// cluster pass: the 2-CTA instances cover the compute-warp shapes of
+// plan_fused; 4- and 8-CTA clusters (rows of 80 / 160 KB: fp64 n = 10000 /
+// 20000) the 8-warp ones
+template <typename T, int CL>
+static int fused2_cw(gf_solver* s, cudaStream_t st, bool attr_only) {
+  const int nv = s->fplan2.nv;
+  if constexpr (CL > 2) {
+    switch (nv) {
+      case 1: case 2: case 3: return fused2_tr<T, 3, 8, CL>(s, st, attr_only);
+      case 4: return fused2_tr<T, 4, 8, CL>(s, st, attr_only);
+      default: return fused2_tr<T, 5, 8, CL>(s, st, attr_only);
+    }
+  } else {
+    switch (s->fplan2.cw) {
+      case 8:
+        switch (nv) {
+          case 1: case 2: case 3: return fused2_tr<T, 3, 8, 2>(s, st, attr_only);
+          case 4: return fused2_tr<T, 4, 8, 2>(s, st, attr_only);
+          default: return fused2_tr<T, 5, 8, 2>(s, st, attr_only);
+        }
+      case 12:
+        return nv == 4 ? fused2_tr<T, 4, 12, 2>(s, st, attr_only) : fused2_tr<T, 5, 12, 2>(s, st, attr_only);
+      case 16:
+        return fused2_tr<T, 4, 16, 2>(s, st, attr_only);
+      default:
+        switch (nv) {
+          case 4: return fused2_tr<T, 4, 20, 2>(s, st, attr_only);
+          case 5: return fused2_tr<T, 5, 20, 2>(s, st, attr_only);
+          default: return fused2_tr<T, 6, 20, 2>(s, st, attr_only);
+        }
+    }
+  }
 }
 
 template <typename T>
 static int fused2_dispatch(gf_solver* s, cudaStream_t st, bool attr_only) {
-  const int nv = s->fplan2.nv;
-  switch (s->fplan2.cw) {
-    case 8:
-      switch (nv) {
-        case 1: case 2: case 3: return fused2_tr<T, 3, 8>(s, st, attr_only);
-        case 4: return fused2_tr<T, 4, 8>(s, st, attr_only);
-        default: return fused2_tr<T, 5, 8>(s, st, attr_only);
-      }
-    case 12:
-      return nv == 4 ? fused2_tr<T, 4, 12>(s, st, attr_only) : fused2_tr<T, 5, 12>(s, st, attr_only);
-    case 16:
-      return fused2_tr<T, 4, 16>(s, st, attr_only);
-    default:
-      switch (nv) {
-        case 4: return fused2_tr<T, 4, 20>(s, st, attr_only);
-        case 5: return fused2_tr<T, 5, 20>(s, st, attr_only);
-        default: return fused2_tr<T, 6, 20>(s, st, attr_only);
-      }
+  switch (s->fplan2.cl) {
+    case 8: return fused2_cw<T, 8>(s, st, attr_only);
+    case 4: return fused2_cw<T, 4>(s, st, attr_only);
+    default: return fused2_cw<T, 2>(s, st, attr_only);
   }
 }
 
@@ -1535,7 +1567,7 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
     s->mark(6, st, false);
     s->mark(5, st, true);
     const unsigned g = (unsigned)(s->fplan.ok ? s->fplan.grid : s->fplan2.grid);
-    const int64_t slabs = s->fplan.ok ? s->fplan.grid : s->fplan2.grid / 2;
+    const int64_t slabs = s->fplan.ok ? s->fplan.grid : s->fplan2.grid / s->fplan2.cl;
     const int64_t nrpart = s->fplan.ok ? (int64_t)s->fplan.ne * s->fplan.grid : (int64_t)s->fplan2.ne * s->fplan2.grid;
     zfinish_kernel<T><<<g, kTailThreads, 0, st>>>(make_ztail<T>(s, slabs, nrpart));
     GF_CHECK_LAUNCH();
@@ -1824,34 +1856,39 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
       if (s->dtype == GF_F32) fused_prepare<float>(s.get());
       else fused_prepare<double>(s.get());
     }
-    // Rows of 40 KB and more: split each row over the two CTAs of a cluster
-    // (gf_fused.cuh, fused_rowcol_cl2_kernel) -- half the bytes per slot,
-    // two rows per group, half the column state per CTA.  GF_FUSED_CL2=0
-    // disables it, =1 forces it for any tall shape (measurements).
+    // Rows of 40 KB and more: split each row over the CTAs of a cluster
+    // (gf_fused.cuh, fused_rowcol_cl_kernel) -- the smallest cluster (2, 4 or
+    // 8 CTAs) that leaves two rows per group and <= 5 vectors per thread:
+    // 2 for fp64 n = 5000 / fp32 n = 10000, 4 for fp64 n = 10000, 8 for fp64
+    // n = 20000 (C3).  GF_FUSED_CL2=0 disables it, =1 forces it for any tall
+    // shape (measurements); GF_FUSED_CL=c picks the cluster size.
     // Not for Newton-prox losses (logistic, negative entropy): one row's prox
     // can take up to 100 Newton steps, and in the single pass every such row
     // stalls its cluster's whole stream, while the two-pass row pass runs the
     // epilogues 32 rows per warp over thousands of warps (measured C2
     // logistic 100000 x 10000 fp32: 1.35 ms cluster pass vs 1.33 two-pass).
     const char* cl2env = getenv("GF_FUSED_CL2");
+    const char* clenv = getenv("GF_FUSED_CL");
     const bool cl2_off = cl2env && cl2env[0] == '0', cl2_force = cl2env && cl2env[0] == '1';
     const bool newton = s->tall && !cl2_force && !cl2_off && one_row && !s->fplan.ok &&
                         has_newton_prox(s->f.view, s->m, st);
     if (s->tall && !cl2_off && !newton && (cl2_force || (one_row && !s->fplan.ok)) &&
         !(env && env[0] == '1')) {
-      s->fplan2 = plan_fused_cl2(s->m, s->ld, (int)es, sms, (size_t)optin, sms / 2, max_slots);
-      if (s->fplan2.ok && (s->fplan2.tr >= 2 || cl2_force)) {
+      for (int cl : {2, 4, 8}) {
+        if (clenv && atoi(clenv) != cl) continue;
+        s->fplan2 = plan_fused_cl(s->m, s->ld, (int)es, sms, (size_t)optin, sms / cl, cl, max_slots);
+        if (!s->fplan2.ok || (s->fplan2.tr < 2 && !cl2_force)) continue;
         const int ncl = s->dtype == GF_F32 ? fused2_dispatch<float>(s.get(), nullptr, true)
                                            : fused2_dispatch<double>(s.get(), nullptr, true);
-        s->fplan2 = plan_fused_cl2(s->m, s->ld, (int)es, sms, (size_t)optin, ncl, max_slots);
-        if (s->fplan2.ok) s->fplan.ok = false;
-      } else {
-        s->fplan2.ok = false;
+        s->fplan2 = plan_fused_cl(s->m, s->ld, (int)es, sms, (size_t)optin, ncl, cl, max_slots);
+        if (s->fplan2.ok) break;
       }
+      if (s->fplan2.ok && (s->fplan2.tr >= 2 || cl2_force)) s->fplan.ok = false;
+      else s->fplan2.ok = false;
     }
   }
   const int64_t nslab = std::max<int64_t>({s->cplan.slabs, s->fplan.ok ? s->fplan.grid : 1,
-                                           s->fplan2.ok ? s->fplan2.grid / 2 : 1});
+                                           s->fplan2.ok ? s->fplan2.grid / s->fplan2.cl : 1});
   vec(s->rpart, std::max<int64_t>({s->grid_r, s->fplan.ok ? kFusedEpiMax * s->fplan.grid : 1,
                                    s->fplan2.ok ? kFusedEpiMax * s->fplan2.grid : 1}) * (kRedY + 1));
   vec(s->xpart, s->grid_s * (kRedX + 1));
