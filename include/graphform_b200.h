@@ -255,6 +255,11 @@ int gf_dense_matvec(int dtype, int64_t m, int64_t n, const void* A, int64_t lda,
                     const double* x, double* y, void* stream);
 /* A_ij <- s_i * (A_ij + t_i) on a DEVICE fp64 matrix (svm generator). */
 int gf_rows_affine(int64_t m, int64_t n, double* A, int64_t lda, const double* s, const double* t, void* stream);
+/* *all_finite <- 1 if every entry of the DEVICE matrix (dtype, m x n, row
+ * stride lda) is finite, else 0: one read of A (the reference's
+ * GraphFormProblem check "A must be finite", problem.py:35-49). */
+int gf_matrix_all_finite(int dtype, int64_t m, int64_t n, const void* A, int64_t lda, int* all_finite,
+                         void* stream);
 /* dst (dtype, row stride ldd) <- src (fp64, row stride lds), DEVICE. */
 int gf_convert_matrix(int64_t m, int64_t n, const double* src, int64_t lds, int dtype, void* dst, int64_t ldd,
                       void* stream);

@@ -107,6 +107,7 @@ _SIGS = {
     "gf_dense_matvec": ([C.c_int, C.c_int64, C.c_int64, _P, C.c_int64, C.c_int, _P, _P, _P], C.c_int),
     "gf_rows_affine": ([C.c_int64, C.c_int64, _P, C.c_int64, _P, _P, _P], C.c_int),
     "gf_convert_matrix": ([C.c_int64, C.c_int64, _P, C.c_int64, C.c_int, _P, C.c_int64, _P], C.c_int),
+    "gf_matrix_all_finite": ([C.c_int, C.c_int64, C.c_int64, _P, C.c_int64, C.POINTER(C.c_int), _P], C.c_int),
     "gf_comm_unique_id": ([C.c_char_p], C.c_int),
     "gf_comm_create": ([C.c_char_p, C.c_int, C.c_int, C.POINTER(_P)], C.c_int),
     "gf_comm_destroy": ([_P], C.c_int),
@@ -340,6 +341,17 @@ def rows_affine(A, s, t):
     s_t, t_t = to_device64(s), to_device64(t)
     check(lib().gf_rows_affine(int(A.shape[0]), int(A.shape[1]), ptr(A), int(A.stride(0)), ptr(s_t), ptr(t_t),
                                stream()))
+
+
+def all_finite(A) -> bool:
+    """Every entry of the CUDA matrix A (unit column stride) finite: one pass
+    over A on the device (gf_matrix_all_finite)."""
+    import torch
+    dt = GF_F32 if A.dtype == torch.float32 else GF_F64
+    out = C.c_int(0)
+    check(lib().gf_matrix_all_finite(dt, int(A.shape[0]), int(A.shape[1]), ptr(A), int(A.stride(0)), C.byref(out),
+                                     stream()))
+    return bool(out.value)
 
 
 def convert_matrix(src, dst):

@@ -324,6 +324,18 @@ static void project_direct(gf_projector* P, const double* c, const double* d, do
 using namespace gf;
 
 struct gf_solver;
+namespace gf {
+// one pass over A: any non-finite entry clears *ok (grid-stride over rows,
+// lanes over columns; no temporaries)
+template <typename T>
+__global__ void all_finite_kernel(const T* __restrict__ A, int64_t m, int64_t n, int64_t lda, int* __restrict__ ok) {
+  bool good = true;
+  for (int64_t r = blockIdx.x; r < m; r += gridDim.x)
+    for (int64_t c = threadIdx.x; c < n; c += blockDim.x) good &= isfinite(A[r * lda + c]);
+  if (!__syncthreads_and(good) && threadIdx.x == 0) atomicExch(ok, 0);
+}
+}  // namespace gf
+
 extern "C" {
 
 const char* gf_version(void) { return "graphform-b200 0.1.0 (sm_100a)"; }
@@ -425,6 +437,24 @@ int gf_rows_affine(int64_t m, int64_t n, double* A, int64_t lda, const double* s
   return guarded(stream, [&] {
     rows_affine(m, n, A, lda, s, t, (cudaStream_t)stream);
     GF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  });
+}
+
+int gf_matrix_all_finite(int dtype, int64_t m, int64_t n, const void* A, int64_t lda, int* all_finite, void* stream) {
+  return guarded(stream, [&] {
+    GF_REQUIRE(dtype == GF_F32 || dtype == GF_F64, GF_E_PARAMETER, "dtype must be GF_F32 or GF_F64");
+    cudaStream_t st = (cudaStream_t)stream;
+    DBuf flag(sizeof(int));
+    const int one = 1;
+    GF_CUDA(cudaMemcpyAsync(flag.p, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+    if (m > 0 && n > 0) {
+      const unsigned g = (unsigned)std::min<int64_t>(m, (int64_t)num_sms() * 16);
+      if (dtype == GF_F32) all_finite_kernel<float><<<g, 256, 0, st>>>((const float*)A, m, n, lda, flag.as<int>());
+      else all_finite_kernel<double><<<g, 256, 0, st>>>((const double*)A, m, n, lda, flag.as<int>());
+      GF_CHECK_LAUNCH();
+    }
+    GF_CUDA(cudaMemcpyAsync(all_finite, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GF_CUDA(cudaStreamSynchronize(st));
   });
 }
 

@@ -11,6 +11,7 @@ Tolerances (stated here):
 
 import numpy as np
 import pytest
+import torch
 
 import paper_1503_08366_b200 as gf
 from oracle import graphform_oracle as orc
@@ -525,3 +526,23 @@ def test_solve_stalled_indirect_wide(name):
     assert np.isfinite(res.objective)
     assert res.objective == pytest.approx(float(fx["objective"]), rel=0.1)
     assert res.primal_residual == pytest.approx(float(fx["r_pri"]), rel=1.0)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_device_matrix_finiteness_check(dtype):
+    """GraphFormProblem on a CUDA matrix checks finiteness in one device pass
+    (gf_matrix_all_finite) with the reference's error (problem.py:35-49):
+    padded row-strided buffers, the last row / column, NaN and inf."""
+    from paper_1503_08366_b200 import instances
+    m, n = 300, 37
+    f = gf.SeparableFunction.uniform(gf.BaseFunction.SQUARE, m)
+    g = gf.SeparableFunction.uniform(gf.BaseFunction.ABS, n)
+    A = instances._dev_matrix(m, n, dtype)          # 128-byte padded rows
+    A.copy_(torch.randn(m, n, dtype=dtype))
+    assert gf.GraphFormProblem(A, f, g).m == m
+    for (i, j, v) in [(m - 1, n - 1, float("nan")), (0, 0, float("inf")), (m // 2, n // 3, float("-inf"))]:
+        B = instances._dev_matrix(m, n, dtype)
+        B.copy_(A)
+        B[i, j] = v
+        with pytest.raises(gf.ParameterError, match="A must be finite"):
+            gf.GraphFormProblem(B, f, g)
