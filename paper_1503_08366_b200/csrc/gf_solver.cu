@@ -1088,6 +1088,7 @@ struct ZTail {
 // the single-GPU in-kernel Z step).
 template <typename T>
 __global__ void __launch_bounds__(kTailThreads) zfinish_kernel(ZTail<T> z) {
+  pdl_trigger();   // the next iteration's G^-1 ring may start its constant-matrix prefetch
   if (z.ctl->status != GF_STATUS_RUNNING) return;
   z.finish();
 }
@@ -1278,7 +1279,10 @@ static bool use_pdl(const gf_solver* s) {
     const char* e = getenv("GF_DISABLE_PDL");
     return e && e[0] == '1';
   }();
-  return !off && !s->profile && !comm_active(s->S->comm);
+  // (under a communicator too: the launches that carry the attribute -- the
+  // G^-1 ring and the fused pass -- follow one of this library's kernels;
+  // the kernels after the NCCL all-reduce are launched without it)
+  return !off && !s->profile;
 }
 
 // attr_only: set the dynamic shared-memory limit of the instance (at create)
