@@ -24,20 +24,29 @@ sq_row_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, int64_t n, cons
               const double* __restrict__ dscale, double* __restrict__ part) {
   // mode 0: Sinkhorn row update (dout = numer / (rs + reg)); mode 1: Frobenius
   // partial sum_i dscale_i^2 * rs_i (no output vector); mode 2: dout = rs.
+  // A warp takes two rows at a time: every weight w_j is loaded once for
+  // both (the weight loads were as many as the matrix loads), eight 16-byte
+  // matrix loads in flight per lane.  Each row's sum is formed in the same
+  // lane order as one row at a time (same bits).
   using V = typename Vec16<T>::type;
   constexpr int VN = Vec16<T>::n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nvec = ld / VN;
   double s_diff = 0.0, s_rows = 0.0, s_bad = 0.0;
-  for (int64_t r = (int64_t)blockIdx.x * kRowWarps + warp; r < rows; r += (int64_t)gridDim.x * kRowWarps) {
-    const V* ar = reinterpret_cast<const V*>(A + r * ld);
-    double acc = 0.0;
-    int64_t v = lane;
-    for (; v < nvec; v += 128) {   // four guarded 16-byte loads issued together per lane
-      V a[4];                      // (unguarded, ptxas scheduled them load-use-load)
+  for (int64_t rp = (int64_t)blockIdx.x * kRowWarps + warp; 2 * rp < rows; rp += (int64_t)gridDim.x * kRowWarps) {
+    const int64_t r0 = 2 * rp;
+    const bool two = r0 + 1 < rows;
+    const V* ar0 = reinterpret_cast<const V*>(A + r0 * ld);
+    const V* ar1 = reinterpret_cast<const V*>(A + (two ? r0 + 1 : r0) * ld);
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int64_t v = lane; v < nvec; v += 128) {   // four guarded 16-byte loads per row issued together
+      V a0[4], a1[4];                              // (unguarded, ptxas scheduled them load-use-load)
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (v + 32 * u < nvec) a[u] = ld_stream(ar + v + 32 * u);
+        if (v + 32 * u < nvec) {
+          a0[u] = ld_stream(ar0 + v + 32 * u);
+          a1[u] = ld_stream(ar1 + v + 32 * u);
+        }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (v + 32 * u >= nvec) break;
@@ -45,29 +54,38 @@ sq_row_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, int64_t n, cons
         for (int i = 0; i < VN; ++i) {
           const int64_t j = (v + 32 * u) * VN + i;
           if (j < n) {
-            const double x = (double)vget(a[u], i);
-            acc = fma(x * x, __ldg(w + j), acc);
+            const double wj = __ldg(w + j);
+            const double x0 = (double)vget(a0[u], i), x1 = (double)vget(a1[u], i);
+            acc0 = fma(x0 * x0, wj, acc0);
+            acc1 = fma(x1 * x1, wj, acc1);
           }
         }
       }
     }
-    acc = warp_sum(acc);
+    acc0 = warp_sum(acc0);
+    acc1 = warp_sum(acc1);
     if (lane == 0) {
-      if (mode == 2) {          // plain weighted row sums of squares: dout = (A o A) w
-        dout[r] = acc;
-        s_rows += acc;
-      } else if (mode == 0) {
-        const double dn = numer / (acc + reg);
-        dout[r] = dn;
-        if (dprev != nullptr) {
-          const double df = dn - dprev[r];
-          s_diff += df * df;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1 && !two) break;
+        const int64_t r = r0 + h;
+        const double acc = h == 0 ? acc0 : acc1;
+        if (mode == 2) {          // plain weighted row sums of squares: dout = (A o A) w
+          dout[r] = acc;
+          s_rows += acc;
+        } else if (mode == 0) {
+          const double dn = numer / (acc + reg);
+          dout[r] = dn;
+          if (dprev != nullptr) {
+            const double df = dn - dprev[r];
+            s_diff += df * df;
+          }
+          if (!(dn > 0.0) || !isfinite(dn)) s_bad += 1.0;
+          s_rows += acc;
+        } else {
+          const double dr = dscale[r];
+          s_rows += (dr * dr) * acc;
         }
-        if (!(dn > 0.0) || !isfinite(dn)) s_bad += 1.0;
-        s_rows += acc;
-      } else {
-        const double dr = dscale[r];
-        s_rows += (dr * dr) * acc;
       }
     }
   }
