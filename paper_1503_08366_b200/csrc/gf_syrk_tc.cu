@@ -817,6 +817,168 @@ syrk_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// ---- pre-split Gram on CTA pairs (tcgen05 cta_group::2; opt-in) -----------
+// The 2-CTA cluster above shares the B panel by multicast, but each SM still
+// takes 24 KB of operands into shared memory per 16-row slab for 128 x 256
+// MACs (ncu: 14.3 ms against a 9 ms f16 floor at 200000 x 5000).  Here the
+// two SMs run ONE 256 x 256
+// MMA (cta_group::2): CTA r holds rows [128 r, 128 r + 128) of the A panel
+// (its TMEM lanes: its half of the tile) and columns [128 r, 128 r + 128) of
+// the B panel, 16 KB per slab per SM for the same MACs per SM.  The leader
+// (rank 0) issues the MMAs; both CTAs' tensor copies (cta_group::2) complete
+// on the leader's `full` barrier; MMA commits are multicast to both CTAs'
+// `empty` / `accf`; each CTA drains its own TMEM half into G and its epilogue
+// warps arrive on the leader's `acce` (count 8).  A stage is four slabs of
+// hi and lo for A and B: one 4-D copy (16-byte K rows of a 128-column panel,
+// column block, 8-row block, hi/lo) per operand.
+constexpr int P2_STAGE = 4 * PRE_SUB * 128 * 16 * 2;      // (A, B) x (hi, lo) x 4 slabs x 2 KB = 64 KB
+constexpr int P2_NST = 3;
+constexpr int P2_SMEM = P2_NST * P2_STAGE;                 // 192 KB
+constexpr uint32_t P2_IDESC = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                              ((uint32_t)(256 >> 4) << 24);   // D f32, A/B f16, K-major, N = 256, M = 256
+
+__device__ __forceinline__ void tma4_cg2(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                         uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5}], [%6];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(leader_bar)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(PRE_THREADS, 1)
+syrk_pre2sm_kernel(const __grid_constant__ CUtensorMap tm, int64_t nkb, int64_t q, int64_t kchunk,
+                   const int2* __restrict__ tiles, double* __restrict__ G, int64_t ldg,
+                   const unsigned* __restrict__ amax_bits) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[P2_NST], empty[P2_NST], accf[2], acce[2];
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const bool leader = rank == 0;
+  const int2 tile = tiles[blockIdx.x >> 1];
+  const int64_t I0 = (int64_t)tile.x * 256, j0 = (int64_t)tile.y * 256;
+  const int64_t i0 = I0 + 128 * rank;                          // this CTA's A rows = TMEM lanes
+  const int64_t nstages = nkb / (2 * PRE_SUB);                 // 8 eight-row blocks (64 rows) per stage
+  const int64_t SPC = kchunk / (BK * PRE_SUB);
+  const int64_t nchunks = (nstages + SPC - 1) / SPC;
+
+  if (tid == 0) {
+    for (int s = 0; s < P2_NST; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      bar_init(&accf[a], 1);
+      bar_init(&acce[a], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base_s)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_s;
+  const uint32_t peer_mask = 0xFEFFFFFFu;                      // shared::cluster address -> the leader's copy
+
+  if (warp == 5) {
+    // ===================== loader (both CTAs) =====================
+    if (lane == 0) {
+      for (int64_t it = 0; it < nstages; ++it) {
+        const int s = (int)(it % P2_NST);
+        if (it >= P2_NST) bar_wait(&empty[s], (unsigned)(((it / P2_NST) - 1) & 1));
+        const uint32_t st = su32(smem + (size_t)s * P2_STAGE);
+        const uint32_t bar = su32(&full[s]) & peer_mask;
+        if (leader)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])),
+                       "r"((unsigned)(2 * P2_STAGE))
+                       : "memory");
+        const int kb = (int)(it * 2 * PRE_SUB);
+        tma4_cg2(st, &tm, 0, (int)(i0 / 128), kb, 0, bar);                              // A rows: hi, lo
+        tma4_cg2(st + P2_STAGE / 2, &tm, 0, (int)(j0 / 128) + (int)rank, kb, 0, bar);     // B half: hi, lo
+      }
+    }
+  } else if (warp == 4) {
+    // ===================== MMA issuer (leader) =====================
+    if (leader && lane == 0) {
+      constexpr uint32_t SL = 2 * PRE_SUB * 128 * 16;          // one operand part (hi or lo): 8 blocks x 2 KB
+      constexpr uint32_t LBO = 128 * 16;                       // next 8-row block
+      for (int64_t c = 0; c < nchunks; ++c) {
+        const int acc = (int)(c & 1);
+        if (c >= 2) bar_wait(&acce[acc], (unsigned)(((c >> 1) - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + (uint32_t)(acc * TN);
+        const int64_t it0 = c * SPC, it1 = min(nstages, it0 + SPC);
+        for (int64_t it = it0; it < it1; ++it) {
+          const int s = (int)(it % P2_NST);
+          bar_wait(&full[s], (unsigned)((it / P2_NST) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a_hi = su32(smem + (size_t)s * P2_STAGE), a_lo = a_hi + SL;
+          const uint32_t b_hi = a_hi + P2_STAGE / 2, b_lo = b_hi + SL;
+#pragma unroll
+          for (int sub = 0; sub < PRE_SUB; ++sub) {            // K = 16: two 8-row blocks per MMA
+            const uint32_t off = (uint32_t)(2 * sub) * LBO;
+            const uint64_t dah = smem_desc(a_hi + off, LBO, 128), dal = smem_desc(a_lo + off, LBO, 128);
+            const uint64_t dbh = smem_desc(b_hi + off, LBO, 128), dbl = smem_desc(b_lo + off, LBO, 128);
+            const uint32_t accum = (it > it0 || sub > 0) ? 1u : 0u;
+#pragma unroll
+            for (int pr = 0; pr < 3; ++pr) {
+              const uint64_t da = pr == 2 ? dal : dah, db = pr == 1 ? dbl : dbh;
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\t"
+                  "setp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                  "l"(da), "l"(db), "r"(P2_IDESC), "r"(pr == 0 ? accum : 1u));
+            }
+          }
+          asm volatile(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  su32(&empty[s])),
+              "h"((uint16_t)3)
+              : "memory");
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                su32(&accf[acc])),
+            "h"((uint16_t)3)
+            : "memory");
+      }
+    }
+    __syncwarp();
+  } else if (warp < 4) {
+    // ===================== epilogue (warps 0-3, both CTAs) =====================
+    const int64_t i = i0 + warp * 32 + lane;
+    const double unscale = ldexp(1.0, -2 * split_shift(amax_bits));
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int acc = (int)(c & 1);
+      bar_wait(&accf[acc], (unsigned)((c >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      drain_chunk(tmem, warp, acc, i, j0, q, G, ldg, unscale);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {   // the leader's acce: local arrive, or a remote one from the peer
+        if (leader) {
+          bar_arrive(&acce[acc]);
+        } else {
+          const uint32_t rb = su32(&acce[acc]) & peer_mask;
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // The kernel accumulates the upper triangle (transposed tile writes); copy it
 // down so callers see the usual lower-triangle result.
 __global__ void upper_to_lower(double* G, int64_t q, int64_t ld) {
@@ -962,7 +1124,63 @@ void gram_tf32x3(const gf_matrix* A, double* G, int64_t ldg, cudaStream_t st, vo
           (const float*)A->data, A->m, A->ld, q, ncp, nkb, amax, (uint4*)hi, (uint4*)lo);
       GF_CHECK_LAUNCH();
       if (verbose) GF_CUDA(cudaEventRecord(ev[1], st));
-      if (cl2) {
+      // GF_SYRK_2SM=1: the cta_group::2 kernel (correct -- the Gram tests pass
+      // on it -- but 18.0 ms against 14.4 ms for the multicast pairs: its
+      // operand reads miss L2 three times as often, 32 GB from DRAM per Gram
+      // against 11 GB, ncu profiles/r02/ncu_syrk_pre2sm.txt)
+      const char* e2 = getenv("GF_SYRK_2SM");
+      const bool two_sm = cl2 && (e2 && e2[0] == '1');
+      if (two_sm) {
+        // 4-D map of the pre-split hi/lo copy (8-byte words): (the 16-byte K rows of
+        // a 128-column block, column block, 8-row block, hi/lo)
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+        if (!encode) {
+          cudaDriverEntryPointQueryResult qr;
+          void* fn = nullptr;
+          GF_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+          GF_REQUIRE(fn != nullptr && qr == cudaDriverEntryPointSuccess, GF_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+          encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+        }
+        const cuuint64_t dims[4] = {256, (cuuint64_t)(ncp / 128), (cuuint64_t)nkb, 2};
+        const cuuint64_t strides[3] = {128 * 16, (cuuint64_t)ncp * 16, (cuuint64_t)pre_bytes};
+        const cuuint32_t box[4] = {256, 1, (cuuint32_t)(2 * PRE_SUB), 2};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        CUtensorMap tm;
+        const CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, scratch, dims, strides, box, estr,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        GF_REQUIRE(r == CUDA_SUCCESS, GF_E_CUDA, "cuTensorMapEncodeTiled (fp16 split) failed");
+        // 256 x 256 tiles (I2, J), J <= I2, column-block major: the pairs in
+        // flight share a B panel (L2 hits; row-major order re-read operands
+        // from DRAM, 37.7 GB per Gram at 200000 x 5000)
+        std::vector<int2> tp;
+        const int64_t nb2 = ceil_div(q, (int64_t)256);
+        for (int64_t bj = 0; bj < nb2; ++bj)
+          for (int64_t bi = bj; bi < nb2; ++bi) tp.push_back(make_int2((int)bi, (int)bj));
+        DBuf d_tp(tp.size() * sizeof(int2));
+        GF_CUDA(cudaMemcpyAsync(d_tp.p, tp.data(), tp.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+        static bool attr2 = false;
+        if (!attr2) {
+          GF_CUDA(cudaFuncSetAttribute(syrk_pre2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
+          attr2 = true;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(2 * tp.size()));
+        cfg.blockDim = dim3(PRE_THREADS);
+        cfg.dynamicSmemBytes = P2_SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        GF_CUDA(cudaLaunchKernelEx(&cfg, syrk_pre2sm_kernel, tm, nkb, q, kchunk, (const int2*)d_tp.as<int2>(), G, ldg,
+                                   (const unsigned*)amax));
+        GF_CHECK_LAUNCH();
+        GF_CUDA(cudaStreamSynchronize(st));   // d_tp is freed on return
+      } else if (cl2) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)tl2.size());
         cfg.blockDim = dim3(PRE_THREADS);
