@@ -219,6 +219,21 @@ static void check_terms(const gf_terms* t) {
   GF_REQUIRE(t->n == 0 || (t->h && t->a && t->b && t->c && t->d && t->e), GF_E_PARAMETER, "null term array");
 }
 
+// lower triangle of a q x q row-major matrix (row stride ld) <-> packed rows
+// (row i: i + 1 entries at i (i + 1) / 2); unpack = 1 writes it back
+__global__ void lower_pack_kernel(double* __restrict__ G, int64_t q, int64_t ld, double* __restrict__ packed,
+                                  int unpack) {
+  const int64_t np = q * (q + 1) / 2;
+  for (int64_t t = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; t < np; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while (i * (i + 1) / 2 > t) --i;
+    while ((i + 1) * (i + 2) / 2 <= t) ++i;
+    const int64_t j = t - i * (i + 1) / 2;
+    if (unpack) G[i * ld + j] = packed[t];
+    else packed[t] = G[i * ld + j];
+  }
+}
+
 static gf_projector* projector_build(gf_matrix* A, int mode, double tol, int64_t max_inner, gf_comm* comm,
                                      cudaStream_t st, const unsigned* amax_known = nullptr) {
   GF_REQUIRE(mode == 0 || mode == 1, GF_E_PARAMETER, "unknown projection mode");
@@ -264,7 +279,19 @@ static gf_projector* projector_build(gf_matrix* A, int mode, double tol, int64_t
   }
   if (gsb > 0) gscratch = sl.get(3, gsb);
   if (A->m > 0 && A->n > 0) gram_accumulate(A, P->tall, P->gram.as<double>(), P->ldg, st, gscratch, gsb, amax_known);
-  if (comm_active(comm)) allreduce_sum(comm, P->gram.as<double>(), (size_t)q * P->ldg, st);
+  if (comm_active(comm)) {
+    // the lower triangle is what every Gram path leaves valid (gram_finish
+    // mirrors it): ship it packed, q (q + 1) / 2 doubles instead of q x ldg
+    const size_t np = (size_t)q * (q + 1) / 2;
+    DBuf packed(std::max<size_t>(np, 1) * sizeof(double));
+    const unsigned g = (unsigned)std::min<int64_t>(ceil_div((int64_t)np, 256), (int64_t)num_sms() * 8);
+    lower_pack_kernel<<<g, 256, 0, st>>>(P->gram.as<double>(), q, P->ldg, packed.as<double>(), 0);
+    GF_CHECK_LAUNCH();
+    allreduce_sum(comm, packed.as<double>(), np, st);
+    lower_pack_kernel<<<g, 256, 0, st>>>(P->gram.as<double>(), q, P->ldg, packed.as<double>(), 1);
+    GF_CHECK_LAUNCH();
+    GF_CUDA(cudaStreamSynchronize(st));   // `packed` is freed on scope exit
+  }
   gram_finish(P->gram.as<double>(), q, P->ldg, st);
   pt.mark("gram");
   // the three q x q fp64 temporaries (arena slots 0-2)

@@ -19,6 +19,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <mutex>
+
 #include "gf_internal.h"
 
 namespace gf {
@@ -525,6 +527,30 @@ int cholesky(double* G, int64_t q, int64_t ld, int* d_info, cudaStream_t st) {
     ev.push_back(e);
   };
   mark();
+  // Depth-1 lookahead: the trailing update of step s is split into (a) the
+  // next panel's columns, on the caller's stream, and (b) the columns after
+  // it, on a second stream -- so potrf(s+1) and trsm(s+1), the serial chain
+  // of small kernels, run while (b)(s) updates the bulk of the trailing
+  // matrix.  (a)(s) waits for (b)(s-1), the other writer of panel s+1's
+  // columns; potrf(s+1) follows (a)(s) in stream order.  (The verbose phase
+  // split keeps one stream.)
+  static std::mutex aux_mu;
+  static cudaStream_t aux_by_dev[64] = {};
+  cudaStream_t aux = nullptr;
+  {
+    int dev = 0;
+    GF_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(aux_mu);
+    if (aux_by_dev[dev & 63] == nullptr) GF_CUDA(cudaStreamCreateWithFlags(&aux_by_dev[dev & 63], cudaStreamNonBlocking));
+    aux = aux_by_dev[dev & 63];
+  }
+  cudaEvent_t ev_t = nullptr, ev_b = nullptr;
+  const bool look = !prof;
+  if (look) {
+    GF_CUDA(cudaEventCreateWithFlags(&ev_t, cudaEventDisableTiming));
+    GF_CUDA(cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming));
+  }
+  bool b_pending = false;
   for (int64_t k0 = 0; k0 < q; k0 += CB) {
     const int nb = (int)std::min<int64_t>(CB, q - k0);
     potrf_block<<<1, 512, kCholSmem, st>>>(G, ld, k0, nb, d_info);
@@ -538,26 +564,35 @@ int cholesky(double* G, int64_t q, int64_t ld, int* d_info, cudaStream_t st) {
     mark();
     double* L21 = G + (k0 + nb) * ld + k0;
     double* G22 = G + (k0 + nb) * ld + k0 + nb;
-    gemm<double, double, false, true>(rest, rest, nb, -1.0, L21, ld, L21, ld, 1.0, G22, ld, true, st);
-    mark();
-  }
-  if (prof) {
-    GF_CUDA(cudaStreamSynchronize(st));
-    double t[3] = {0, 0, 0};
-    for (size_t i = 1; i < ev.size(); ++i) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
-      t[(i - 1) % 3] += ms;
+    if (!look) {
+      gemm<double, double, false, true>(rest, rest, nb, -1.0, L21, ld, L21, ld, 1.0, G22, ld, true, st);
+      mark();
+      continue;
     }
-    fprintf(stderr, "[gf] cholesky q=%lld: potrf %.2f ms, trsm %.2f ms, update %.2f ms\n", (long long)q, t[0], t[1],
-            t[2]);
-    for (auto e : ev) cudaEventDestroy(e);
+    const int64_t na = std::min<int64_t>(CB, rest);   // (a): the next panel's columns, every row below
+    const int64_t rb = rest - na;                       // (b): the columns after it
+    if (rb > 0) {
+      GF_CUDA(cudaEventRecord(ev_t, st));               // L21 of this step is final
+      GF_CUDA(cudaStreamWaitEvent(aux, ev_t, 0));
+    }
+    if (b_pending) GF_CUDA(cudaStreamWaitEvent(st, ev_b, 0));   // (b) of the previous step
+    gemm<double, double, false, true>(rest, na, nb, -1.0, L21, ld, L21, ld, 1.0, G22, ld, true, st);
+    b_pending = false;
+    if (rb > 0) {
+      const double* L21b = L21 + na * ld;
+      gemm<double, double, false, true>(rb, rb, nb, -1.0, L21b, ld, L21b, ld, 1.0, G22 + na * ld + na, ld, true, aux);
+      GF_CUDA(cudaEventRecord(ev_b, aux));
+      b_pending = true;
+    }
   }
+  if (look && b_pending) GF_CUDA(cudaStreamWaitEvent(st, ev_b, 0));
   zero_upper<<<grid2(q), dim3(32, 8), 0, st>>>(G, q, ld);
   GF_CHECK_LAUNCH();
   int info = 0;
   GF_CUDA(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, st));
   GF_CUDA(cudaStreamSynchronize(st));
+  if (ev_t) cudaEventDestroy(ev_t);
+  if (ev_b) cudaEventDestroy(ev_b);
   return info;
 }
 

@@ -7,7 +7,8 @@ library owns an NCCL communicator (built from a unique id that rank 0 creates
 and ``torch.distributed`` broadcasts) and issues
 
   setup      one all-reduce per Sinkhorn sweep (n column sums + scalars),
-             one for the Frobenius rescale, one of the Gram matrix;
+             one for the Frobenius rescale, one of the Gram matrix (packed
+             lower triangle);
   iteration  ONE all-reduce of 2*ld + 8 doubles between the column pass and
              the controller: [A_hat' c_y | A_hat' nu^ | r_pri^2, ||y||^2,
              f(y), drift, flags, and the two gap terms]; every rank then
