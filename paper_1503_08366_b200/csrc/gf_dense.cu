@@ -516,7 +516,7 @@ int cholesky(double* G, int64_t q, int64_t ld, int* d_info, cudaStream_t st) {
     GF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   GF_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), st));
-  const char* vb = getenv("GF_VERBOSE_SETUP");
+  const char* vb = getenv("GF_VERBOSE_CHOL");   // potrf / trsm / update split (one stream)
   const bool prof = vb && vb[0] == '1';
   std::vector<cudaEvent_t> ev;
   auto mark = [&]() {
@@ -534,21 +534,33 @@ int cholesky(double* G, int64_t q, int64_t ld, int* d_info, cudaStream_t st) {
   // matrix.  (a)(s) waits for (b)(s-1), the other writer of panel s+1's
   // columns; potrf(s+1) follows (a)(s) in stream order.  (The verbose phase
   // split keeps one stream.)
+  // The chain (potrf, trsm, next panel) runs on a high-priority stream so its
+  // small grids are scheduled ahead of the bulk update's remaining CTAs.
   static std::mutex aux_mu;
-  static cudaStream_t aux_by_dev[64] = {};
-  cudaStream_t aux = nullptr;
+  static cudaStream_t aux_by_dev[64] = {}, crit_by_dev[64] = {};
+  cudaStream_t aux = nullptr, crit = nullptr;
   {
     int dev = 0;
     GF_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(aux_mu);
-    if (aux_by_dev[dev & 63] == nullptr) GF_CUDA(cudaStreamCreateWithFlags(&aux_by_dev[dev & 63], cudaStreamNonBlocking));
+    if (aux_by_dev[dev & 63] == nullptr) {
+      int lo = 0, hi = 0;
+      GF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      GF_CUDA(cudaStreamCreateWithPriority(&aux_by_dev[dev & 63], cudaStreamNonBlocking, lo));
+      GF_CUDA(cudaStreamCreateWithPriority(&crit_by_dev[dev & 63], cudaStreamNonBlocking, hi));
+    }
     aux = aux_by_dev[dev & 63];
+    crit = crit_by_dev[dev & 63];
   }
   cudaEvent_t ev_t = nullptr, ev_b = nullptr;
   const bool look = !prof;
+  cudaStream_t caller = st;
   if (look) {
     GF_CUDA(cudaEventCreateWithFlags(&ev_t, cudaEventDisableTiming));
     GF_CUDA(cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming));
+    GF_CUDA(cudaEventRecord(ev_t, caller));   // G and d_info are ready
+    GF_CUDA(cudaStreamWaitEvent(crit, ev_t, 0));
+    st = crit;
   }
   bool b_pending = false;
   for (int64_t k0 = 0; k0 < q; k0 += CB) {
@@ -586,6 +598,11 @@ int cholesky(double* G, int64_t q, int64_t ld, int* d_info, cudaStream_t st) {
     }
   }
   if (look && b_pending) GF_CUDA(cudaStreamWaitEvent(st, ev_b, 0));
+  if (look) {   // back on the caller's stream
+    GF_CUDA(cudaEventRecord(ev_t, crit));
+    GF_CUDA(cudaStreamWaitEvent(caller, ev_t, 0));
+    st = caller;
+  }
   zero_upper<<<grid2(q), dim3(32, 8), 0, st>>>(G, q, ld);
   GF_CHECK_LAUNCH();
   int info = 0;
