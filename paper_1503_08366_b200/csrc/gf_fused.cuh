@@ -55,6 +55,10 @@ constexpr int kFusedEpiMax = 8;
 __host__ __device__ constexpr int fused_epi(int cw) { return GF_FUSED_NE; }
 // CTA size for CW compute warps: + the epilogue warps + 1 producer warp
 __host__ __device__ constexpr int fused_threads(int cw) { return (cw + fused_epi(cw) + 1) * 32; }
+// The lagged cluster pass (below) runs more epilogue warps.
+constexpr int kLagEpi = 7;
+__host__ __device__ constexpr int fused_epi_lag(int cw, int lag) { return lag > 0 ? kLagEpi : fused_epi(cw); }
+__host__ __device__ constexpr int fused_threads_lag(int cw, int lag) { return (cw + fused_epi_lag(cw, lag) + 1) * 32; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -137,6 +141,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
+}
+
+// The same without a cache-policy hint (normal L2 priority).
+__device__ __forceinline__ void bulk_g2s_nohint(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
 __device__ __forceinline__ float vdot(const float4& a, const float4& b, float s) {
@@ -645,9 +657,19 @@ __device__ __forceinline__ void st_async_f64(uint32_t cluster_addr, double v, ui
                "d"(v), "r"(cluster_bar)
                : "memory");
 }
+__device__ __forceinline__ void st_async_t(uint32_t cluster_addr, double v, uint32_t cluster_bar) {
+  st_async_f64(cluster_addr, v, cluster_bar);
+}
+__device__ __forceinline__ void st_async_t(uint32_t cluster_addr, float v, uint32_t cluster_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(cluster_addr),
+               "f"(v), "r"(cluster_bar)
+               : "memory");
+}
 
 struct FusedPlan2 {
   int cl = 0;          // CTAs per cluster (2, 4 or 8): each streams 1/cl of every row
+  int lag = 0;         // > 0: column pass on rows re-read from L2, lag groups behind (nslotc C-ring slots)
+  int nslotc = 0;
   int cw = 0, ne = 0, nv = 0, nslot = 0, tr = 0;
   int grid = 0;        // CTAs (cl per cluster)
   int64_t hvec = 0;    // 16-byte vectors of the widest share of a row (the slot size)
@@ -662,9 +684,10 @@ __host__ __device__ inline int64_t cl_vec_begin(int64_t nvec, int rank, int cl) 
 // (cudaOccupancyMaxActiveClusters): the kernel is persistent, every cluster
 // must be resident in one wave.
 inline FusedPlan2 plan_fused_cl(int64_t m, int64_t ld, int esize, int sms, size_t smem_max, int max_clusters, int cl,
-                                int max_slots = kMaxSlots) {
+                                int max_slots = kMaxSlots, int lag = 0) {
   FusedPlan2 p;
   p.cl = cl;
+  p.lag = lag;
   const int vn = 16 / esize;
   const int64_t nvec = ld / vn;
   p.hvec = ceil_div(nvec, (int64_t)cl);
@@ -672,12 +695,18 @@ inline FusedPlan2 plan_fused_cl(int64_t m, int64_t ld, int esize, int sms, size_
   for (int cw : {8, 12, 16, 20})
     if (ceil_div(p.hvec, cw * 32) <= (cw <= 12 ? 5 : 4)) { p.cw = cw; break; }
   p.nv = (int)ceil_div(p.hvec, p.cw * 32);
-  p.ne = fused_epi(p.cw);
+  p.ne = fused_epi_lag(p.cw, lag);
   const size_t slot_bytes = (size_t)p.hvec * 16;
   const size_t budget = smem_max > kStaticSmemReserve ? smem_max - kStaticSmemReserve : 0;
   p.nslot = (int)std::min<size_t>(std::min(max_slots, kMaxSlots), budget / slot_bytes);
   const int want_pf = std::max<int>(2, (int)ceil_div(48 * 1024, (int64_t)slot_bytes));
   p.tr = 0;
+  if (lag > 0) {   // two rows per group; C ring: the group being read + one prefetched; R ring: the rest
+    p.tr = 2;
+    p.nslotc = 4;   // (6 measured the same on C2)
+    p.nslot -= p.nslotc;
+    if (p.nslot < p.tr + 2) p.tr = 0;
+  } else
   for (int tr : {4, 2, 1})   // (2 TR (cl - 1) partials per group go out on distinct lanes)
     if ((3 * tr + want_pf <= p.nslot || (tr == 1 && 3 + 1 <= p.nslot)) && 2 * tr * (cl - 1) <= 32) {
       p.tr = tr;
@@ -685,20 +714,33 @@ inline FusedPlan2 plan_fused_cl(int64_t m, int64_t ld, int esize, int sms, size_
     }
   const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms / cl, (int64_t)max_clusters, m}));
   p.grid = (int)(cl * ncl);
-  p.smem = (size_t)p.nslot * slot_bytes;
+  p.smem = (size_t)(p.nslot + p.nslotc) * slot_bytes;
   // every CTA needs a non-empty share
   const bool shares = nvec >= cl && cl_vec_begin(nvec, 1, cl) >= 1;
   p.ok = max_clusters >= 1 && shares && p.nv >= 1 && p.nv <= 6 && p.tr >= 1 && m > 0 &&
-         (cl == 2 || p.cw == 8);   // (the 4- and 8-CTA instances exist for 8 compute warps)
+         (cl == 2 || p.cw == 8) &&   // (the 4- and 8-CTA instances exist for 8 compute warps,
+         (lag == 0 || (cl == 2 && p.cw == 8));   //  the lagged one for 2-CTA clusters of 8)
   return p;
 }
 
 // CL CTAs per cluster (2, 4, 8; the cluster shape is a launch attribute).
-template <typename T, int NV, int TR, int CW, int CL, class Epi, class Tail = NoTail>
-__global__ void __launch_bounds__(fused_threads(CW), 1)
+//
+// LAG > 0 (heavy epilogues: Newton-prox losses): the column pass does not keep
+// the rows in shared memory.  R(t) releases its slots at once; the producer
+// re-reads the rows of group t - LAG from global memory (L2: the LAG groups
+// of rows in between are a few tens of MB chip-wide) into a second ring, and
+// C(t - LAG) runs on those.  Each CTA runs the epilogue of its own rows only
+// and st.async-writes their weights into the peer too, and there are
+// kLagEpi epilogue warps: a logistic prox is ~8 fp64 Newton steps, and the
+// stream delivers ~1.2 rows per us per SM, so several rows must be in their
+// Newton loop at once.  The weights live in a ring of LAG + 1 entries.
+// nslot: R-ring slots; nslotc: C-ring slots (LAG > 0 only).
+
+template <typename T, int NV, int TR, int CW, int CL, class Epi, class Tail = NoTail, int LAG = 0>
+__global__ void __launch_bounds__(fused_threads_lag(CW, LAG), 1)
 fused_rowcol_cl_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const T* __restrict__ x0,
                        const T* __restrict__ x1, Epi epi, int nslot, int64_t hvec, double* __restrict__ rpart,
-                       double* __restrict__ cpart, Tail tail = Tail{}) {
+                       double* __restrict__ cpart, Tail tail = Tail{}, int nslotc = 0) {
   using V = typename Vec16<T>::type;
   constexpr int VN = Vec16<T>::n;
   constexpr int NR = Epi::NR;
@@ -706,7 +748,7 @@ fused_rowcol_cl_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const 
   constexpr int LGK = K == 2 ? 1 : (K == 4 ? 2 : 3);
   constexpr int kFusedWarps = CW;
   constexpr int kFusedThreads = CW * kWarp;
-  constexpr int NE = fused_epi(CW);
+  constexpr int NE = fused_epi_lag(CW, LAG);
   constexpr int kEpiWarp = CW;
   constexpr int kProdWarp = CW + NE;
   static_assert(CW <= 32, "one epilogue lane per compute warp");
@@ -714,9 +756,12 @@ fused_rowcol_cl_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const 
   __shared__ __align__(8) uint64_t full[kMaxSlots], sfree[kMaxSlots];
   static_assert(CL == 2 || CL == 4 || CL == 8, "cluster of 2, 4 or 8 CTAs");
   static_assert(K * (CL - 1) <= 32, "one lane per (value, peer) partial");
-  __shared__ __align__(8) uint64_t redf[NE], rede[NE], wf[NE], we[NE], xf[NE][2];
+  constexpr int WR = LAG > 0 ? LAG + 1 : NE;   // weight buffers: group g uses w_s[g % WR]
+  constexpr int CLAG = LAG > 0 ? LAG : 2;      // the column pass of group t - CLAG runs after R(t)
+  __shared__ __align__(8) uint64_t redf[NE], rede[NE], wf[WR], we[WR], xf[NE][2];
+  __shared__ __align__(8) uint64_t fullc[LAG > 0 ? kMaxSlots : 1], freec[LAG > 0 ? kMaxSlots : 1];
   __shared__ T red_s[NE][kFusedWarps][K];
-  __shared__ __align__(8) T w_s[NE][TR][2];
+  __shared__ __align__(8) T w_s[WR][TR][2];
   __shared__ __align__(8) double xbuf[NE][2][CL][K];   // [buffer][use parity][source rank][value]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -740,11 +785,18 @@ fused_rowcol_cl_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const 
     for (int b = 0; b < NE; ++b) {
       mbar_init(&redf[b], kFusedWarps);
       mbar_init(&rede[b], 1);
-      mbar_init(&wf[b], 1);
-      mbar_init(&we[b], kFusedWarps);
       mbar_init(&xf[b][0], 1);
       mbar_init(&xf[b][1], 1);
     }
+    for (int b = 0; b < WR; ++b) {
+      mbar_init(&wf[b], 1);
+      mbar_init(&we[b], kFusedWarps);
+    }
+    if constexpr (LAG > 0)
+      for (int s = 0; s < nslotc; ++s) {
+        mbar_init(&fullc[s], 1);
+        mbar_init(&freec[s], kFusedWarps);
+      }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -757,19 +809,47 @@ fused_rowcol_cl_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const 
       const int pre = min(nslot, nr);
       for (int j = 0; j < pre; ++j) {
         mbar_arrive_expect_tx(&full[j], cb);
-        bulk_g2s(smem_raw + j * sb, A + (r0 + j) * ld + v0 * VN, cb, &full[j], pol);
+        if constexpr (LAG > 0) bulk_g2s_nohint(smem_raw + j * sb, A + (r0 + j) * ld + v0 * VN, cb, &full[j]);
+        else bulk_g2s(smem_raw + j * sb, A + (r0 + j) * ld + v0 * VN, cb, &full[j], pol);
       }
       pdl_wait();
       pdl_trigger();
       if (!epi.active()) {
         for (int j = 0; j < pre; ++j) mbar_wait(&full[j], 0u);
-      } else {
+      } else if constexpr (LAG == 0) {
         int slot = pre == nslot ? 0 : pre;
         for (int j = pre; j < nr; ++j) {
           if (j >= nslot) mbar_wait(&sfree[slot], (unsigned)(((j / nslot) - 1) & 1));
           mbar_arrive_expect_tx(&full[slot], cb);
           bulk_g2s(smem_raw + slot * sb, A + (r0 + j) * ld + v0 * VN, cb, &full[slot], pol);
           if (++slot == nslot) slot = 0;
+        }
+      } else {
+        // R loads at normal L2 priority: the line is read again LAG groups
+        // later, by lane 1's column-ring loads below
+        int slot = pre == nslot ? 0 : pre;
+        for (int j = pre; j < nr; ++j) {
+          if (j >= nslot) mbar_wait(&sfree[slot], (unsigned)(((j / nslot) - 1) & 1));
+          mbar_arrive_expect_tx(&full[slot], cb);
+          bulk_g2s_nohint(smem_raw + slot * sb, A + (r0 + j) * ld + v0 * VN, cb, &full[slot]);
+          if (++slot == nslot) slot = 0;
+        }
+      }
+    }
+    if constexpr (LAG > 0) {
+      // lane 1: the column-ring re-loads (evict-first: their last use), on
+      // their own so that waiting for a column slot never holds back the
+      // HBM row stream.  (Lanes 0 and 1 diverge; both spin on try_wait.)
+      if (lane == 1 && epi.active()) {
+        pdl_wait();
+        const uint64_t pol = policy_evict_first();
+        unsigned char* ringc = smem_raw + (size_t)nslot * sb;
+        int slotc = 0;
+        for (int jc = 0; jc < nr; ++jc) {
+          if (jc >= nslotc) mbar_wait(&freec[slotc], (unsigned)(((jc / nslotc) - 1) & 1));
+          mbar_arrive_expect_tx(&fullc[slotc], cb);
+          bulk_g2s(ringc + slotc * sb, A + (r0 + jc) * ld + v0 * VN, cb, &fullc[slotc], pol);
+          if (++slotc == nslotc) slotc = 0;
         }
       }
     }
@@ -791,7 +871,7 @@ fused_rowcol_cl_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const 
       const bool sender = lane < K * (CL - 1);
       const uint32_t xb_peer = mapa_u32(smem_u32(&xbuf[b][0][rank][sq]), speer);   // my slot in the peer's buffer
       const uint32_t xf_peer = mapa_u32(smem_u32(&xf[b][0]), speer);
-      const uint32_t xf_loc = smem_u32(&xf[b][0]), we_loc = smem_u32(&we[b]), redf_loc = smem_u32(&redf[b]);
+      const uint32_t xf_loc = smem_u32(&xf[b][0]), redf_loc = smem_u32(&redf[b]);
       constexpr uint32_t kUseStride = (uint32_t)(CL * K * sizeof(double));   // xbuf[b][1] - xbuf[b][0]
       typename Epi::RowIn in{};
       if (lane < TR && par * TR + lane < nr) in = epi.load_in(r0 + par * TR + lane);
@@ -839,14 +919,41 @@ fused_rowcol_cl_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const 
         const bool mine = lane < g && ((ge * TR + lane) % CL == (int)rank);
         typename Epi::Mid md{};
         double w0 = 0.0, w1 = 0.0;
-        if (lane < g) md = epi.mid(in, dots, w0, w1);
-        if (use >= 1) mbar_wait_u32(we_loc, (use - 1) & 1u);    // w_s[b] consumed by C(ge - NE)
-        if (lane < g) {
-          w_s[b][lane][0] = (T)w0;
-          w_s[b][lane][1] = (T)w1;
+        const int gw = ge % WR;
+        const unsigned wuse = (unsigned)(ge / WR);
+        if constexpr (LAG == 0) {
+          if (lane < g) md = epi.mid(in, dots, w0, w1);
+          if (wuse >= 1) mbar_wait_u32(smem_u32(&we[gw]), (wuse - 1) & 1u);    // w_s[gw] consumed by C(ge - WR)
+          if (lane < g) {
+            w_s[gw][lane][0] = (T)w0;
+            w_s[gw][lane][1] = (T)w1;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive_expect_tx(&wf[gw], 0);
+        } else {
+          // own rows only; their weights also go to the peer's w_s[gw] by
+          // st.async (wf[gw]: the local arrival + the peer's bytes).  The peer
+          // writes group ge only after it has this CTA's partials of ge, sent
+          // after R(ge), which follows C(ge - WR) in this CTA's compute warps:
+          // the slot is free by construction.
+          static_assert(CL == 2 && TR % 2 == 0, "lagged pass: 2-CTA clusters, even TR");
+          if (mine) md = epi.mid(in, dots, w0, w1);
+          if (wuse >= 1) mbar_wait_u32(smem_u32(&we[gw]), (wuse - 1) & 1u);
+          if (mine) {
+            w_s[gw][lane][0] = (T)w0;
+            w_s[gw][lane][1] = (T)w1;
+            const uint32_t peer = rank ^ 1u;
+            const uint32_t pw = mapa_u32(smem_u32(&w_s[gw][lane][0]), peer);
+            const uint32_t pf = mapa_u32(smem_u32(&wf[gw]), peer);
+            st_async_t(pw, (T)w0, pf);
+            st_async_t(pw + (uint32_t)sizeof(T), (T)w1, pf);
+          }
+          __syncwarp();
+          int own = 0;   // the peer's rows of this group: g - own, two values each
+#pragma unroll
+          for (int rr = 0; rr < TR; ++rr) own += (rr < g && ((ge * TR + rr) % CL == (int)rank)) ? 1 : 0;
+          if (lane == 0) mbar_arrive_expect_tx(&wf[gw], (unsigned)((g - own) * 2 * sizeof(T)));
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(&wf[b], 0);
         if (mine) epi.tail(r0 + (int64_t)ge * TR + lane, in, dots, md, ered, eflags);
         const int jn = (ge + NE) * TR + lane;
         if (lane < TR && jn < nr) in = epi.load_in(r0 + jn);
@@ -891,11 +998,13 @@ fused_rowcol_cl_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const 
       const bool red_writer = (lane & ((32 >> LGK) - 1)) == 0;
       T* const red_dst = &red_s[0][warp][lane >> (5 - LGK)];
       int slotR = 0, slotC = 0;
-      unsigned phaseR = 0;
+      unsigned phaseR = 0, phaseC = 0;
       int jR = 0, jC = 0;
       int bR = 0, bC = 0;
       unsigned useR = 0, useC = 0;
-      for (int t = 0; t < ng + 2; ++t) {
+      const uint32_t ringc0 = ring0 + (uint32_t)nslot * sb;
+      const uint32_t fullc0 = smem_u32(fullc), freec0 = smem_u32(freec);
+      for (int t = 0; t < ng + CLAG; ++t) {
         if (t < ng) {   // ---- R(t) ----
           T s[K];
 #pragma unroll
@@ -912,6 +1021,10 @@ fused_rowcol_cl_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const 
                 p0[v] = dot_acc(a, xa[v]);
                 p1[v] = dot_acc(a, xb[v]);
               }
+              if constexpr (LAG > 0) {   // the row is re-read from L2 for the column pass
+                __syncwarp();
+                if (lane == 0) mbar_arrive_u32(sfree0 + 8u * slotR);
+              }
 #pragma unroll
               for (int v = 1; v < NV; ++v) { p0[0] = dot_add(p0[0], p0[v]); p1[0] = dot_add(p1[0], p1[v]); }
               s[2 * rr] = dot_fin(p0[0]);
@@ -927,18 +1040,24 @@ fused_rowcol_cl_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const 
           if (lane == 0) mbar_arrive_u32(redf0 + 8u * bR);
           if (++bR == NE) { bR = 0; ++useR; }
         }
-        if (t >= 2) {   // ---- C(t-2) ----
+        if (t >= CLAG) {   // ---- C(t - CLAG) ----
           mbar_wait_u32(wf0 + 8u * bC, useC & 1u);
           T w0[TR], w1[TR];
 #pragma unroll
           for (int rr = 0; rr < TR; ++rr) { w0[rr] = w_s[bC][rr][0]; w1[rr] = w_s[bC][rr][1]; }
           __syncwarp();
           if (lane == 0) mbar_arrive_u32(we0 + 8u * bC);
-          if (++bC == NE) { bC = 0; ++useC; }
+          if (++bC == WR) { bC = 0; ++useC; }
 #pragma unroll
           for (int rr = 0; rr < TR; ++rr) {
             if (jC < nr) {
-              const uint32_t row = ring0 + (uint32_t)slotC * sb;
+              uint32_t row;
+              if constexpr (LAG > 0) {
+                mbar_wait_u32(fullc0 + 8u * slotC, phaseC);
+                row = ringc0 + (uint32_t)slotC * sb;
+              } else {
+                row = ring0 + (uint32_t)slotC * sb;
+              }
 #pragma unroll
               for (int v = 0; v < NV; ++v) {
                 const V a = lds128(row + voff[v], (V*)nullptr);
@@ -946,9 +1065,13 @@ fused_rowcol_cl_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const 
                 vaxpy(cb2[v], a, w1[rr]);
               }
               __syncwarp();
-              if (lane == 0) mbar_arrive_u32(sfree0 + 8u * slotC);
+              if (lane == 0) mbar_arrive_u32((LAG > 0 ? freec0 : sfree0) + 8u * slotC);
               ++jC;
-              if (++slotC == nslot) slotC = 0;
+              if constexpr (LAG > 0) {
+                if (++slotC == nslotc) { slotC = 0; phaseC ^= 1u; }
+              } else {
+                if (++slotC == nslot) slotC = 0;
+              }
             }
           }
         }

@@ -1369,13 +1369,13 @@ static void fused_dispatch(gf_solver* s, cudaStream_t st, bool attr_only) {
 
 // Two-CTA cluster variant.  attr_only: set the shared-memory limit and
 // return the number of co-resident clusters of this instance.
-template <typename T, int NV, int TR, int CW, int CL>
+template <typename T, int NV, int TR, int CW, int CL, int LAG = 0>
 static int fused2_go(gf_solver* s, cudaStream_t st, bool attr_only) {
   const FusedPlan2& p = s->fplan2;
-  auto kern = fused_rowcol_cl_kernel<T, NV, TR, CW, CL, YEpi<T>, ZTail<T>>;
+  auto kern = fused_rowcol_cl_kernel<T, NV, TR, CW, CL, YEpi<T>, ZTail<T>, LAG>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(attr_only ? CL * (num_sms() / CL) : p.grid));
-  cfg.blockDim = dim3(fused_threads(CW));
+  cfg.blockDim = dim3(fused_threads_lag(CW, LAG));
   cfg.dynamicSmemBytes = p.smem;
   cfg.stream = st;
   cudaLaunchAttribute at[2];
@@ -1397,7 +1397,8 @@ static int fused2_go(gf_solver* s, cudaStream_t st, bool attr_only) {
   cfg.numAttrs = use_pdl(s) ? 2 : 1;
   GF_CUDA(cudaLaunchKernelEx(&cfg, kern, (const T*)s->S->A->data, s->m, s->ld, (const T*)s->xk_T.as<T>(),
                              (const T*)s->xh_T.as<T>(), make_yepi<T>(s), p.nslot, p.hvec, s->rpart.as<double>(),
-                             s->cpart.as<double>(), make_ztail<T>(s, p.grid / CL, (int64_t)p.ne * p.grid)));
+                             s->cpart.as<double>(), make_ztail<T>(s, p.grid / CL, (int64_t)p.ne * p.grid),
+                             p.nslotc));
   GF_CHECK_LAUNCH();
   return 0;
 }
@@ -1441,8 +1442,21 @@ static int fused2_cw(gf_solver* s, cudaStream_t st, bool attr_only) {
   }
 }
 
+// Lagged cluster pass for Newton-prox losses (gf_fused.cuh, LAG): 2-CTA
+// clusters of 8 compute warps, two rows per group.  C2 (fp32 logistic
+// 100000 x 10000) per pass: lag 4 0.950 ms, 6 0.892, 8 0.885, 12 0.907,
+// 16 1.11 (the re-read rows no longer stay in L2).
+constexpr int kNewtonLag = 8;
+
 template <typename T>
 static int fused2_dispatch(gf_solver* s, cudaStream_t st, bool attr_only) {
+  if (s->fplan2.lag > 0) {
+    switch (s->fplan2.nv) {
+      case 1: case 2: case 3: return fused2_go<T, 3, 2, 8, 2, kNewtonLag>(s, st, attr_only);
+      case 4: return fused2_go<T, 4, 2, 8, 2, kNewtonLag>(s, st, attr_only);
+      default: return fused2_go<T, 5, 2, 8, 2, kNewtonLag>(s, st, attr_only);
+    }
+  }
   switch (s->fplan2.cl) {
     case 8: return fused2_cw<T, 8>(s, st, attr_only);
     case 4: return fused2_cw<T, 4>(s, st, attr_only);
@@ -1866,25 +1880,31 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
     // 2 for fp64 n = 5000 / fp32 n = 10000, 4 for fp64 n = 10000, 8 for fp64
     // n = 20000 (C3).  GF_FUSED_CL2=0 disables it, =1 forces it for any tall
     // shape (measurements); GF_FUSED_CL=c picks the cluster size.
-    // Not for Newton-prox losses (logistic, negative entropy): one row's prox
-    // can take up to 100 Newton steps, and in the single pass every such row
-    // stalls its cluster's whole stream, while the two-pass row pass runs the
-    // epilogues 32 rows per warp over thousands of warps (measured C2
-    // logistic 100000 x 10000 fp32: 1.35 ms cluster pass vs 1.33 two-pass).
+    // Newton-prox losses (logistic, negative entropy: ~8 fp64 Newton steps
+    // per row, up to 100) take the lagged variant (kNewtonLag): with the rows
+    // kept in shared memory every slow prox stalls its cluster's stream
+    // (C2 logistic 100000 x 10000 fp32: 1.35 ms, vs 1.32 ms two-pass); with
+    // the column pass re-reading rows from L2 kNewtonLag groups behind and
+    // seven epilogue warps, 0.95 ms.  GF_FUSED_LAG=0 turns it off (two-pass),
+    // =1 forces it for any loss (tests).  2-CTA clusters only: fp64 n = 10000
+    // stays two-pass.
     const char* cl2env = getenv("GF_FUSED_CL2");
     const char* clenv = getenv("GF_FUSED_CL");
     const bool cl2_off = cl2env && cl2env[0] == '0', cl2_force = cl2env && cl2env[0] == '1';
+    const char* lagenv = getenv("GF_FUSED_LAG");
     const bool newton = s->tall && !cl2_force && !cl2_off && one_row && !s->fplan.ok &&
                         has_newton_prox(s->f.view, s->m, st);
-    if (s->tall && !cl2_off && !newton && (cl2_force || (one_row && !s->fplan.ok)) &&
+    const bool lag_on = lagenv ? lagenv[0] == '1' : newton;
+    if (s->tall && !cl2_off && (!newton || lag_on) && (cl2_force || (one_row && !s->fplan.ok)) &&
         !(env && env[0] == '1')) {
+      const int lag = lag_on ? kNewtonLag : 0;
       for (int cl : {2, 4, 8}) {
-        if (clenv && atoi(clenv) != cl) continue;
-        s->fplan2 = plan_fused_cl(s->m, s->ld, (int)es, sms, (size_t)optin, sms / cl, cl, max_slots);
+        if ((clenv && atoi(clenv) != cl) || (lag && cl != 2)) continue;
+        s->fplan2 = plan_fused_cl(s->m, s->ld, (int)es, sms, (size_t)optin, sms / cl, cl, max_slots, lag);
         if (!s->fplan2.ok || (s->fplan2.tr < 2 && !cl2_force)) continue;
         const int ncl = s->dtype == GF_F32 ? fused2_dispatch<float>(s.get(), nullptr, true)
                                            : fused2_dispatch<double>(s.get(), nullptr, true);
-        s->fplan2 = plan_fused_cl(s->m, s->ld, (int)es, sms, (size_t)optin, ncl, cl, max_slots);
+        s->fplan2 = plan_fused_cl(s->m, s->ld, (int)es, sms, (size_t)optin, ncl, cl, max_slots, lag);
         if (s->fplan2.ok) break;
       }
       if (s->fplan2.ok && (s->fplan2.tr >= 2 || cl2_force)) s->fplan.ok = false;

@@ -3,7 +3,8 @@ two-pass schedule (GF_DISABLE_FUSED=1, what wide rows and Newton-heavy
 problems use), the plain row GEMV for G^-1 (GF_DISABLE_RING=1), the cluster
 pass forced onto these narrow rows with 2-, 4- and 8-CTA clusters
 (GF_FUSED_CL2=1, GF_FUSED_CL=c: the instances that C5 fp64 and C3 use at
-full size), and launches without programmatic dependent launch
+full size), its lagged form (GF_FUSED_LAG=1: column pass on rows re-read
+from L2, what C2's logistic loss uses), and launches without programmatic dependent launch
 (GF_DISABLE_PDL=1, bit-identical).  Each variant runs in a subprocess (the
 switches are read once per process)."""
 
@@ -27,7 +28,7 @@ import numpy as np
 import paper_1503_08366_b200 as gf
 from tests import _cases
 out = {}
-for name in ("lasso_tall_20000x500", "svm_2000x100", "lp_600x240"):
+for name in ("lasso_tall_20000x500", "svm_2000x100", "lp_600x240", "logistic_1000x100_fixed"):
     fx = _cases.load("solve_" + name)
     r = gf.solve(_cases.build_problem(fx), gf.SolverSettings(**_cases.settings_of(fx)))
     out[name] = {"it": r.iterations, "status": r.status.value, "x": r.x.tolist(), "y": r.y.tolist(),
@@ -51,11 +52,16 @@ def test_schedule_variants_agree():
     assert nopdl == base   # PDL changes launch timing only: bit-identical
     for env in ({"GF_DISABLE_FUSED": "1"}, {"GF_DISABLE_RING": "1"},
                 {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "2"}, {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "4"},
-                {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "8"}):
+                {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "8"},
+                {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "2", "GF_FUSED_LAG": "1"}):
         alt = run_variant(env)
         for name, b in base.items():
             a = alt[name]
             assert a["it"] == b["it"] and a["status"] == b["status"], (env, name)
             for k in ("x", "y"):
-                np.testing.assert_allclose(a[k], b[k], rtol=1e-9, atol=1e-11, err_msg=f"{env} {name} {k}")
-            assert a["obj"] == pytest.approx(b["obj"], rel=1e-10)
+                # the logistic case: its 1000 fixed-rho iterations amplify
+                # summation-order differences to ~1e-6 relative; checked at the
+                # tolerance of the parity test against the reference (1e-5)
+                rtol, atol = (1e-5, 1e-8) if name.startswith("logistic") else (1e-9, 1e-11)
+                np.testing.assert_allclose(a[k], b[k], rtol=rtol, atol=atol, err_msg=f"{env} {name} {k}")
+            assert a["obj"] == pytest.approx(b["obj"], rel=1e-5 if name.startswith("logistic") else 1e-10)

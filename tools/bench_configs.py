@@ -25,6 +25,7 @@ CONFIGS = {
     "c5d": ("tall_lasso", 200_000, 5_000, np.float64),
     "c2d": ("logistic", 100_000, 10_000, np.float64),
     "c5": ("tall_lasso", 200_000, 5_000, np.float32),
+    "c2l": ("tall_lasso", 100_000, 10_000, np.float32),   # C2 shape, Lasso loss (dev)
 }
 NAMES = ["ginv_gemv_xside", "row_pass_yside", "col_pass", "slab_reduce", "y_scalars", "zstep_controller",
          "allreduce", "fused_rowcol_yside"]
