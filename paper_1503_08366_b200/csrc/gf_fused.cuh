@@ -754,7 +754,7 @@ fused_rowcol_cl_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const 
   static_assert(CW <= 32, "one epilogue lane per compute warp");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxSlots], sfree[kMaxSlots];
-  static_assert(CL == 2 || CL == 4 || CL == 8, "cluster of 2, 4 or 8 CTAs");
+  static_assert(CL == 2 || CL == 4 || CL == 8 || CL == 9, "cluster of 2, 4, 8 or 9 CTAs");
   static_assert(K * (CL - 1) <= 32, "one lane per (value, peer) partial");
   constexpr int WR = LAG > 0 ? LAG + 1 : NE;   // weight buffers: group g uses w_s[g % WR]
   constexpr int CLAG = LAG > 0 ? LAG : 2;      // the column pass of group t - CLAG runs after R(t)

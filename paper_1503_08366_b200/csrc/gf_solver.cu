@@ -1409,8 +1409,8 @@ static int fused2_tr(gf_solver* s, cudaStream_t st, bool attr_only) {
 }
 
 // cluster pass: the 2-CTA instances cover the compute-warp shapes of
-// plan_fused; 4- and 8-CTA clusters (rows of 80 / 160 KB: fp64 n = 10000 /
-// 20000) the 8-warp ones
+// plan_fused; 4-, 8- and 9-CTA clusters (rows of 80 / 160 KB: fp64 n = 10000
+// / 20000) the 8-warp ones
 template <typename T, int CL>
 static int fused2_cw(gf_solver* s, cudaStream_t st, bool attr_only) {
   const int nv = s->fplan2.nv;
@@ -1458,6 +1458,7 @@ static int fused2_dispatch(gf_solver* s, cudaStream_t st, bool attr_only) {
     }
   }
   switch (s->fplan2.cl) {
+    case 9: return fused2_cw<T, 9>(s, st, attr_only);
     case 8: return fused2_cw<T, 8>(s, st, attr_only);
     case 4: return fused2_cw<T, 4>(s, st, attr_only);
     default: return fused2_cw<T, 2>(s, st, attr_only);
@@ -1576,7 +1577,7 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
     // scalars, then the all-reduce and the rest of the Z step
     s->mark(7, st, true);
     if (s->fplan.ok) launch_fused<T>(s, st);
-    else fused2_dispatch<T>(s, st, false);   // rows split over 2-CTA clusters
+    else fused2_dispatch<T>(s, st, false);   // rows split over the CTAs of a cluster
     s->mark(7, st, false);
     s->launches += 1;
     if (!comm_active(s->S->comm)) return;
@@ -1875,11 +1876,12 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
       else fused_prepare<double>(s.get());
     }
     // Rows of 40 KB and more: split each row over the CTAs of a cluster
-    // (gf_fused.cuh, fused_rowcol_cl_kernel) -- the smallest cluster (2, 4 or
-    // 8 CTAs) that leaves two rows per group and <= 5 vectors per thread:
-    // 2 for fp64 n = 5000 / fp32 n = 10000, 4 for fp64 n = 10000, 8 for fp64
-    // n = 20000 (C3).  GF_FUSED_CL2=0 disables it, =1 forces it for any tall
-    // shape (measurements); GF_FUSED_CL=c picks the cluster size.
+    // (gf_fused.cuh, fused_rowcol_cl_kernel) -- of the cluster sizes (2, 4,
+    // 8 or 9 CTAs) that leave two rows per group and <= 5 vectors per thread,
+    // the one with the most co-resident SMs: 2 for fp64 n = 5000 / fp32
+    // n = 10000, 4 for fp64 n = 10000, 9 for fp64 n = 20000 (C3; 8 would
+    // leave 28 SMs idle).  GF_FUSED_CL2=0 disables it, =1 forces it for any
+    // tall shape (measurements); GF_FUSED_CL=c picks the cluster size.
     // Newton-prox losses (logistic, negative entropy: ~8 fp64 Newton steps
     // per row, up to 100) take the lagged variant (kNewtonLag): with the rows
     // kept in shared memory every slow prox stalls its cluster's stream
@@ -1898,17 +1900,34 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
     if (s->tall && !cl2_off && (!newton || lag_on) && (cl2_force || (one_row && !s->fplan.ok)) &&
         !(env && env[0] == '1')) {
       const int lag = lag_on ? kNewtonLag : 0;
-      for (int cl : {2, 4, 8}) {
+      // every cluster size that fits; the one that keeps the most SMs busy
+      // wins (a larger cluster only for >= 5 % more: its exchange costs more).
+      // Co-resident clusters of c CTAs on a 148-SM B200 (one CTA per SM,
+      // tools/cluster_probe.cu): 2 -> 148 SMs, 4 -> 132, 8 -> 120, 9 -> 135.
+      FusedPlan2 best;
+      for (int cl : {2, 4, 8, 9}) {
         if ((clenv && atoi(clenv) != cl) || (lag && cl != 2)) continue;
         s->fplan2 = plan_fused_cl(s->m, s->ld, (int)es, sms, (size_t)optin, sms / cl, cl, max_slots, lag);
         if (!s->fplan2.ok || (s->fplan2.tr < 2 && !cl2_force)) continue;
         const int ncl = s->dtype == GF_F32 ? fused2_dispatch<float>(s.get(), nullptr, true)
                                            : fused2_dispatch<double>(s.get(), nullptr, true);
         s->fplan2 = plan_fused_cl(s->m, s->ld, (int)es, sms, (size_t)optin, ncl, cl, max_slots, lag);
-        if (s->fplan2.ok) break;
+        if (s->fplan2.ok && (!best.ok || 20 * (int64_t)s->fplan2.grid >= 21 * (int64_t)best.grid)) best = s->fplan2;
       }
+      s->fplan2 = best;
       if (s->fplan2.ok && (s->fplan2.tr >= 2 || cl2_force)) s->fplan.ok = false;
       else s->fplan2.ok = false;
+    }
+    const char* vb = getenv("GF_VERBOSE_SETUP");
+    if (vb && vb[0] == '1') {
+      if (s->fplan.ok)
+        fprintf(stderr, "[gf] iteration: fused pass, grid %d, %d compute warps, %d rows per group, %d slots\n",
+                s->fplan.grid, s->fplan.cw, s->fplan.tr, s->fplan.nslot);
+      else if (s->fplan2.ok)
+        fprintf(stderr, "[gf] iteration: cluster pass, %d-CTA clusters, grid %d, %d rows per group, %d slots, lag %d\n",
+                s->fplan2.cl, s->fplan2.grid, s->fplan2.tr, s->fplan2.nslot, s->fplan2.lag);
+      else
+        fprintf(stderr, "[gf] iteration: two-pass schedule\n");
     }
   }
   const int64_t nslab = std::max<int64_t>({s->cplan.slabs, s->fplan.ok ? s->fplan.grid : 1,

@@ -1,9 +1,9 @@
 """The alternative iteration schedules agree with the default one: the
 two-pass schedule (GF_DISABLE_FUSED=1, what wide rows and Newton-heavy
 problems use), the plain row GEMV for G^-1 (GF_DISABLE_RING=1), the cluster
-pass forced onto these narrow rows with 2-, 4- and 8-CTA clusters
+pass forced onto these narrow rows with 2-, 4-, 8- and 9-CTA clusters
 (GF_FUSED_CL2=1, GF_FUSED_CL=c: the instances that C5 fp64 and C3 use at
-full size), its lagged form (GF_FUSED_LAG=1: column pass on rows re-read
+full size; 9 is C3's), its lagged form (GF_FUSED_LAG=1: column pass on rows re-read
 from L2, what C2's logistic loss uses), and launches without programmatic dependent launch
 (GF_DISABLE_PDL=1, bit-identical).  Each variant runs in a subprocess (the
 switches are read once per process)."""
@@ -52,7 +52,7 @@ def test_schedule_variants_agree():
     assert nopdl == base   # PDL changes launch timing only: bit-identical
     for env in ({"GF_DISABLE_FUSED": "1"}, {"GF_DISABLE_RING": "1"},
                 {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "2"}, {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "4"},
-                {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "8"},
+                {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "8"}, {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "9"},
                 {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "2", "GF_FUSED_LAG": "1"}):
         alt = run_variant(env)
         for name, b in base.items():
