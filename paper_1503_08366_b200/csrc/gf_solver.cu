@@ -38,6 +38,9 @@
 #include "gf_gemv.cuh"
 #include "gf_fused.cuh"
 #include "gf_ring.cuh"
+#include "gf_sym.cuh"
+
+#include <cudaTypedefs.h>
 
 namespace gf {
 
@@ -56,6 +59,7 @@ struct Ctl {
   double gap;          // duality gap of the last gap test (solver.py:378-390)
   int64_t gap_set;     // 1 once a gap was computed
   unsigned gcnt, ggen; // grid barrier of the fused pass's Z tail (arrivals, generation)
+  unsigned scnt, sgen; // grid barrier of the lower-triangle G^-1 GEMV (gf_sym.cuh)
 };
 
 struct Params {
@@ -1192,6 +1196,9 @@ struct gf_solver {
   FusedPlan fplan;
   FusedPlan2 fplan2;  // two-CTA cluster variant (rows of 40 KB and more)
   RingPlan rplan;     // S step on the TMA row ring (tall, direct)
+  SymPlan splan;      // S step on the lower triangle of G^-1 (tall, direct; preferred)
+  CUtensorMap sym_tm; // 64 x 64 tiles of G^-1
+  DBuf sympart;       // per-tile row / column partials of the S step
   int warm_x = 0;
   int64_t next_step = 0;  // step k = [S(k-1)], R(k), C(k), Z(k)
   Ctl host{};
@@ -1481,6 +1488,45 @@ static void ring_go(gf_solver* s, cudaStream_t st, bool attr_only) {
 }
 
 template <typename T>
+static void sym_go(gf_solver* s, cudaStream_t st, bool attr_only) {
+  const SymPlan& p = s->splan;
+  auto kern = sym_gemv_kernel<T, XEpi<T>>;
+  if (attr_only) {
+    GF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    return;
+  }
+  launch_k(use_pdl(s), kern, dim3(p.grid), dim3(sym_threads<T>()), p.smem, st, s->sym_tm, s->q,
+           (const T*)s->rhs_T.as<T>(), make_xepi<T>(s), p.nslot, p.nb, p.nt, s->sympart.as<double>(),
+           &s->ctl.as<Ctl>()->scnt, &s->ctl.as<Ctl>()->sgen, s->xpart.as<double>(), s->grid_s);
+}
+
+// 2-D tensor map over G^-1 (q columns x q rows, row stride ldq): 64 x 64
+// boxes, zero fill past q in both directions.  The driver entry point comes
+// through the runtime (no libcuda link dependency).
+static CUtensorMap sym_map(const void* g, int64_t q, int64_t ldq, int dtype) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult qr;
+    void* fn = nullptr;
+    GF_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+    GF_REQUIRE(fn != nullptr && qr == cudaDriverEntryPointSuccess, GF_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const size_t es = dtype == GF_F32 ? 4 : 8;
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)q, (cuuint64_t)q};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ldq * es)};
+  const cuuint32_t box[2] = {(cuuint32_t)kSymTB, (cuuint32_t)kSymTB};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&m, dtype == GF_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                            const_cast<void*>(g), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  GF_REQUIRE(r == CUDA_SUCCESS, GF_E_CUDA, "cuTensorMapEncodeTiled (G^-1 tiles) failed");
+  return m;
+}
+
+template <typename T>
 static void ring_dispatch(gf_solver* s, cudaStream_t st, bool attr_only) {
   const int nv = s->rplan.nv;
   switch (s->rplan.cw) {
@@ -1562,7 +1608,8 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
     s->launches += 1;
   } else if (k > 0) {  // S(k-1): x+ = Ginv rhs and the x side of iteration k
     s->mark(0, st, true);
-    if (s->rplan.ok) ring_dispatch<T>(s, st, false);
+    if (s->splan.ok) sym_go<T>(s, st, false);
+    else if (s->rplan.ok) ring_dispatch<T>(s, st, false);
     else
     launch_k(use_pdl(s), rowgemv_kernel<T, 1, XEpi<T>>, dim3((unsigned)s->grid_s), dim3(kRowThreads), 0, st,
              (const T*)P->ginv.as<T>(), s->q, s->ldq, (const T*)s->rhs_T.as<T>(), (const T*)s->rhs_T.as<T>(),
@@ -1853,6 +1900,17 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
     if (s->rplan.ok) {
       if (s->dtype == GF_F32) ring_dispatch<float>(s.get(), nullptr, true);
       else ring_dispatch<double>(s.get(), nullptr, true);
+    }
+    {   // the lower-triangle S step (gf_sym.cuh) replaces both when it fits
+      const char* senv = getenv("GF_DISABLE_SYM");
+      if (!(senv && senv[0] == '1') && s->tall && !s->indirect && s->ldq > 0)
+        s->splan = plan_sym(s->q, s->ldq, (int)es, sms, (size_t)optin, s->grid_s);
+      if (s->splan.ok) {
+        s->sym_tm = sym_map(s->S->P->ginv.p, s->q, s->ldq, s->dtype);
+        s->sympart.alloc((size_t)s->splan.nt * 2 * kSymTB * sizeof(double));
+        if (s->dtype == GF_F32) sym_go<float>(s.get(), nullptr, true);
+        else sym_go<double>(s.get(), nullptr, true);
+      }
     }
     // GF_FUSED_MAXSLOTS (dev): cap the ring slots -- compute-sanitizer's
     // synccheck tracks a bounded number of mbarriers per CTA

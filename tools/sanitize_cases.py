@@ -34,7 +34,7 @@ elif case in ("fused64", "twopass", "equil"):
     prob, _ = instances.tall_lasso(3000, 700, 0, device=True)
     st = gf.SolverSettings(max_iter=6)
 elif case in ("cl2", "cl9"):
-    prob, _ = instances.tall_lasso(6000, 5000, 0, device=True)
+    prob, _ = instances.tall_lasso(int(os.environ.get("SAN_M", "6000")), 5000, 0, device=True)
     st = gf.SolverSettings(max_iter=4)
 elif case == "lag":
     prob, _ = instances.generate(instances.GenSpec("logistic", 10500, 10000, 0), device=True)
