@@ -294,8 +294,15 @@ static gf_projector* projector_build(gf_matrix* A, int mode, double tol, int64_t
   }
   gram_finish(P->gram.as<double>(), q, P->ldg, st);
   pt.mark("gram");
-  // the three q x q fp64 temporaries (arena slots 0-2)
-  DBufView L(sl.get(0, gbytes)), tmp(sl.get(1, gbytes)), inv(sl.get(2, gbytes));
+  // q x q fp64 temporaries: the factor L (arena slot 0) and one buffer that
+  // is first TRTRI's scratch and then, once W = L^-1 is formed in place, the
+  // W'W output.  For an fp64 matrix that buffer is G^-1 itself (same padded
+  // stride): 9.6 GB instead of 16 GB of q x q buffers at C3's q = 20000, so
+  // a first build stays inside the pool's pre-mapped reserve.
+  const bool direct = A->dtype == GF_F64 && P->ldq == P->ldg;
+  if (direct) P->ginv.alloc(gbytes);
+  DBufView L(sl.get(0, gbytes)), tmp(direct ? P->ginv.p : sl.get(1, gbytes));
+  DBufView& inv = tmp;
   DBuf info(sizeof(int));
   GF_CUDA(cudaMemcpyAsync(L.p, P->gram.p, gbytes, cudaMemcpyDeviceToDevice, st));
   const int bad = cholesky(L.as<double>(), q, P->ldg, info.as<int>(), st);
@@ -307,8 +314,10 @@ static gf_projector* projector_build(gf_matrix* A, int mode, double tol, int64_t
   trtri(L.as<double>(), q, P->ldg, tmp.as<double>(), st);
   pt.mark("trtri");
   inverse_from_factor_inv(L.as<double>(), q, P->ldg, inv.as<double>(), st);
-  P->ginv.alloc((size_t)std::max<int64_t>(q, 1) * P->ldq * A->esize());
-  store_matrix(inv.as<double>(), P->ldg, A->dtype, P->ginv.p, P->ldq, q, q, st);
+  if (!direct) {
+    P->ginv.alloc((size_t)std::max<int64_t>(q, 1) * P->ldq * A->esize());
+    store_matrix(inv.as<double>(), P->ldg, A->dtype, P->ginv.p, P->ldq, q, q, st);
+  }
   pt.mark("inverse");
   GF_CUDA(cudaStreamSynchronize(st));
   pt.report("projector_build");

@@ -220,6 +220,136 @@ __global__ void __launch_bounds__(256) dgemm_tc_kernel(int64_t M, int64_t N, int
   }
 }
 
+// ---------------------------------------- pipelined fp64 tensor-core GEMM --
+// The DMMA GEMM above stages one 16-deep K slice with a register prefetch:
+// at q = 20000 TRTRI and W'W ran at 19-25 TF/s, the slice's global latency
+// exposed behind 64 DMMAs per warp.  This one streams K slices through a
+// PST-stage cp.async ring (16-byte copies, zero-filled past M / N / K) into
+// 128 x 128 tiles: 8 warps as 2 x 4, a 64 x 32 warp tile = 8 x 4 DMMA.8x8x4
+// tiles, 64 fp64 accumulators per thread, 12 fragment loads per 32 DMMAs.
+// Every operand is staged in its global orientation -- k-contiguous rows
+// [mn][k] (stride PKC = 20 doubles, 4 mod 16) or mn-contiguous rows [k][mn]
+// (stride PMC = 136, 8 mod 16) -- both of which serve the m8n8k4 fragment
+// pattern (8 mn x 4 k per warp) in the minimum two wavefronts.  The DMMA
+// sequence over k (k4 steps in increasing order, the same kbeg / kend) is
+// the old kernel's, so the two produce identical results.
+constexpr int PBM = 128, PBK = 16, PST = 4, PMC = PBM + 8, PKC = PBK + 4;
+constexpr int PSTAGE = PBM * PKC > PBK * PMC ? PBM * PKC : PBK * PMC;   // doubles per operand stage
+constexpr size_t kPipeSmem = (size_t)PST * 2 * PSTAGE * sizeof(double);
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+
+// one PBM x PBK operand stage: KC = rows of the tile contiguous in k
+// (X[mn * ld + k]), else contiguous in mn (X[k * ld + mn])
+template <bool KC>
+__device__ __forceinline__ void pipe_stage(double* S, const double* __restrict__ X, int64_t ld, int64_t mn0,
+                                           int64_t MN, int64_t k0, int64_t K, int tid) {
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int c = s * 256 + tid;
+    int r, e;   // stage row, element
+    int64_t mn, k;
+    if (KC) { r = c >> 3; e = (c & 7) * 2; mn = mn0 + r; k = k0 + e; }
+    else { r = c >> 6; e = (c & 63) * 2; k = k0 + r; mn = mn0 + e; }
+    int valid = 0;
+    if (mn < MN && k < K) valid = KC ? (K - k >= 2 ? 2 : 1) : (MN - mn >= 2 ? 2 : 1);
+    const double* src = valid ? (KC ? X + mn * ld + k : X + k * ld + mn) : X;
+    cp_async16(S + (KC ? r * PKC + e : r * PMC + e), src, valid * 8);
+  }
+}
+
+template <bool AT, bool BT>
+__global__ void __launch_bounds__(256, 1) dgemm_pipe_kernel(int64_t M, int64_t N, int64_t K, double alpha,
+                                                            const double* __restrict__ A, int64_t lda, int64_t sA,
+                                                            const double* __restrict__ B, int64_t ldb, int64_t sB,
+                                                            double beta, double* __restrict__ C, int64_t ldc,
+                                                            int64_t sC, int lower_only, int kmode) {
+  constexpr bool AKC = !AT, BKC = BT;   // A[i*lda+k] is k-contiguous; B[j*ldb+k] (BT) too
+  const int64_t i0 = (int64_t)blockIdx.y * PBM, j0 = (int64_t)blockIdx.x * PBM;
+  if (lower_only && j0 > i0 + PBM - 1) return;
+  // kmode as in dgemm_tc_kernel, in TBK (16) units: the same DMMA sequence
+  const int64_t kbeg = kmode == 1 ? (j0 / TBK) * TBK : (kmode == 3 ? (i0 / TBK) * TBK : 0);
+  const int64_t kend = kmode == 2 ? min(K, i0 + PBM) : K;
+  A += blockIdx.z * sA;
+  B += blockIdx.z * sB;
+  C += blockIdx.z * sC;
+  extern __shared__ __align__(16) double psm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int fk = lane & 3, fr = lane >> 2;
+  const int64_t nk = kend > kbeg ? (kend - kbeg + PBK - 1) / PBK : 0;
+  auto SA = [&](int64_t s) { return psm + (size_t)(s % PST) * 2 * PSTAGE; };
+  auto SB = [&](int64_t s) { return psm + (size_t)(s % PST) * 2 * PSTAGE + PSTAGE; };
+#pragma unroll
+  for (int s = 0; s < PST - 1; ++s) {
+    if (s < nk) {
+      pipe_stage<AKC>(SA(s), A, lda, i0, M, kbeg + s * PBK, K, tid);
+      pipe_stage<BKC>(SB(s), B, ldb, j0, N, kbeg + s * PBK, K, tid);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int64_t it = 0; it < nk; ++it) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(PST - 2) : "memory");
+    __syncthreads();   // stage it landed for every thread; stage it - 1 is free
+    const int64_t nx = it + PST - 1;
+    if (nx < nk) {
+      pipe_stage<AKC>(SA(nx), A, lda, i0, M, kbeg + nx * PBK, K, tid);
+      pipe_stage<BKC>(SB(nx), B, ldb, j0, N, kbeg + nx * PBK, K, tid);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const double* sa = SA(it);
+    const double* sb = SB(it);
+#pragma unroll
+    for (int ks = 0; ks < PBK / 4; ++ks) {
+      const int k = ks * 4 + fk;
+      double fa[8], fb[4];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int m = wm * 64 + t * 8 + fr;
+        fa[t] = AKC ? sa[m * PKC + k] : sa[k * PMC + m];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int n = wn * 32 + u * 8 + fr;
+        fb[u] = BKC ? sb[n * PKC + k] : sb[k * PMC + n];
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], fa[t], fb[u]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int64_t gi = i0 + wm * 64 + t * 8 + fr;
+    if (gi >= M) continue;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gj = j0 + wn * 32 + u * 8 + fk * 2 + h;
+        if (gj >= N) continue;
+        double* c = C + gi * ldc + gj;
+        *c = beta == 0.0 ? alpha * acc[t][u][h] : alpha * acc[t][u][h] + beta * *c;
+      }
+  }
+}
+
+static bool pipe_ok(const void* A, int64_t lda, int64_t sA, const void* B, int64_t ldb, int64_t sB) {
+  return ((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0 && lda % 2 == 0 && ldb % 2 == 0 && sA % 2 == 0 &&
+         sB % 2 == 0;
+}
+
 template <typename TA, typename TB, bool AT, bool BT>
 static void gemm(int64_t M, int64_t N, int64_t K, double alpha, const TA* A, int64_t lda,
                  const TB* B, int64_t ldb, double beta, double* C, int64_t ldc, bool lower,
@@ -234,6 +364,23 @@ static void gemm(int64_t M, int64_t N, int64_t K, double alpha, const TA* A, int
     // 128-deep Cholesky trailing updates) are faster on the SIMT tile, whose
     // smaller CTAs fill the machine better (measured at q = 5000 and 20000;
     // at q = 20000 DMMA for the updates: 160 -> 245 ms)
+    static const int pipe_mink = [] {   // GF_DGEMM_PIPE_MINK: K from which the pipelined kernel runs (0: never)
+      const char* e = getenv("GF_DGEMM_PIPE_MINK");
+      return e ? atoi(e) : 512;
+    }();
+    if (!simt && pipe_mink > 0 && K >= pipe_mink && pipe_ok(A, lda, sA, B, ldb, sB)) {
+      static bool attr = false;
+      if (!attr) {
+        GF_CUDA(cudaFuncSetAttribute(dgemm_pipe_kernel<AT, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kPipeSmem));
+        attr = true;
+      }
+      dim3 grid((unsigned)ceil_div(N, PBM), (unsigned)ceil_div(M, PBM), (unsigned)batch);
+      dgemm_pipe_kernel<AT, BT><<<grid, 256, kPipeSmem, st>>>(M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C,
+                                                              ldc, sC, lower ? 1 : 0, kmode);
+      GF_CHECK_LAUNCH();
+      return;
+    }
     if (!simt && K >= 512) {
       dim3 grid((unsigned)ceil_div(N, TBN), (unsigned)ceil_div(M, TBM), (unsigned)batch);
       dgemm_tc_kernel<AT, BT><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC,
