@@ -710,6 +710,73 @@ int cholesky(double* G, int64_t q, int64_t ld, int* d_info, cudaStream_t st) {
     st = crit;
   }
   bool b_pending = false;
+  // Two-level blocking (GF_CHOL_SP; default 512 from q = 8192, else one level): columns go
+  // in super-panels of SP.  Inside one, each 128-column step updates only the
+  // super-panel's later columns (every row below: the next steps' TRSM needs
+  // them); the trailing matrix past the super-panel takes all SP columns'
+  // contributions in one K = SP product, long enough for the pipelined DMMA
+  // GEMM (30 TF/s at K = 512 against ~16 for the 128-deep SIMT updates).
+  // The lookahead is the one-level scheme's at super-panel granularity: (a)
+  // the next super-panel's columns on the chain stream, (b) the rest on aux.
+  // Measured (C3, q = 20000): one level 175-205 ms, SP = 512 164 ms, 256 and
+  // 1024 slower (529 / 377 ms: K below the pipelined kernel's range, resp.
+  // a longer serial chain); at q = 5000 one level is faster (7.0 vs 7.4 ms).
+  static const int64_t sp_env = [] {
+    const char* e = getenv("GF_CHOL_SP");
+    return e ? (int64_t)atoll(e) : (int64_t)-1;
+  }();
+  const int64_t sp_req = sp_env >= 0 ? sp_env : (q >= 8192 ? 512 : 0);
+  const int64_t SP = sp_req >= 2 * CB && sp_req % CB == 0 ? sp_req : 0;
+  if (SP > 0 && q > SP) {
+    for (int64_t K0 = 0; K0 < q; K0 += SP) {
+      const int64_t pe = std::min<int64_t>(K0 + SP, q);
+      for (int64_t k0 = K0; k0 < pe; k0 += CB) {
+        const int nb = (int)std::min<int64_t>(CB, q - k0);
+        potrf_block<<<1, 512, kCholSmem, st>>>(G, ld, k0, nb, d_info);
+        GF_CHECK_LAUNCH();
+        mark();
+        const int64_t rest = q - k0 - nb;
+        if (rest <= 0) break;
+        const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(rest, 16), sms);
+        trsm_rows<<<grid, 512, kCholSmem, st>>>(G, ld, q, k0, nb);
+        GF_CHECK_LAUNCH();
+        mark();
+        const int64_t wc = pe - (k0 + nb);   // the super-panel's later columns
+        if (wc > 0) {
+          double* L21 = G + (k0 + nb) * ld + k0;
+          gemm<double, double, false, true>(rest, wc, nb, -1.0, L21, ld, L21, ld, 1.0, G + (k0 + nb) * ld + k0 + nb,
+                                            ld, true, st);
+          mark();
+        }
+      }
+      const int64_t rest = q - pe;
+      if (rest <= 0) break;
+      const int64_t kw = pe - K0;
+      const double* L21 = G + pe * ld + K0;
+      double* G22 = G + pe * ld + pe;
+      if (!look) {
+        gemm<double, double, false, true>(rest, rest, kw, -1.0, L21, ld, L21, ld, 1.0, G22, ld, true, st);
+        mark();
+        continue;
+      }
+      const int64_t na = std::min<int64_t>(SP, rest);
+      const int64_t rb = rest - na;
+      if (rb > 0) {
+        GF_CUDA(cudaEventRecord(ev_t, st));
+        GF_CUDA(cudaStreamWaitEvent(aux, ev_t, 0));
+      }
+      if (b_pending) GF_CUDA(cudaStreamWaitEvent(st, ev_b, 0));
+      gemm<double, double, false, true>(rest, na, kw, -1.0, L21, ld, L21, ld, 1.0, G22, ld, true, st);
+      b_pending = false;
+      if (rb > 0) {
+        const double* L21b = L21 + na * ld;
+        gemm<double, double, false, true>(rb, rb, kw, -1.0, L21b, ld, L21b, ld, 1.0, G22 + na * ld + na, ld, true,
+                                          aux);
+        GF_CUDA(cudaEventRecord(ev_b, aux));
+        b_pending = true;
+      }
+    }
+  } else
   for (int64_t k0 = 0; k0 < q; k0 += CB) {
     const int nb = (int)std::min<int64_t>(CB, q - k0);
     potrf_block<<<1, 512, kCholSmem, st>>>(G, ld, k0, nb, d_info);
