@@ -722,7 +722,14 @@ int gf_setup_create(gf_matrix* A, int equil, const double* d_in, const double* e
       PhaseTimer pt(st);
       const EquilResult r = equilibrate(A, -1.0, -1.0, 300, comm, S->d.as<double>(), S->e.as<double>(), st);
       pt.mark("equilibrate");
-      rescale_even(A, S->d.as<double>(), S->e.as<double>(), comm, st);
+      // the Frobenius norm comes from the last sweep's column sums (no pass
+      // over A; GF_RESCALE_PASS=1 forms it with rescale_even's row pass)
+      static const bool pass = [] {
+        const char* ev = getenv("GF_RESCALE_PASS");
+        return ev && ev[0] == '1';
+      }();
+      if (r.fro2 >= 0.0 && !pass) rescale_even_fro2(A, S->d.as<double>(), S->e.as<double>(), r.fro2, comm, st);
+      else rescale_even(A, S->d.as<double>(), S->e.as<double>(), comm, st);
       pt.mark("rescale");
       pt.report("setup");
       S->info.sweeps = r.sweeps;

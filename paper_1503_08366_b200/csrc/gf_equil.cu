@@ -140,6 +140,20 @@ __global__ void sum_parts(const double* __restrict__ part, int64_t count, int st
   }
 }
 
+// out = sum_j a_j b_j, one CTA, fixed order
+__global__ void fro2_dot_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n, double* out) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += a[i] * b[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
 __global__ void sqrt_inplace(double* x, int64_t n) {
   for (int64_t j = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
     x[j] = sqrt(x[j]);
@@ -252,11 +266,19 @@ static EquilResult equil_t(gf_matrix* A, double gamma, double eps, int64_t max_i
   // the last row update is in d_it unless we swapped after it
   const double* d_last = converged ? d_it : d_prev;
   if (m > 0) GF_CUDA(cudaMemcpyAsync(d_out, d_last, m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  // ||D A E||_F^2 = sum_i d_i sum_j a_ij^2 e_j = sum_j e_j csum_j (squared
+  // scalings; csum: the last sweep's column sums, made with the final d) --
+  // rescale_even's norm without another pass over A
+  fro2_dot_kernel<<<1, 256, 0, st>>>(e, csum.as<double>(), n, scal.as<double>() + 5);
   sqrt_inplace<<<vgrid(m), 256, 0, st>>>(d_out, m);
   sqrt_inplace<<<vgrid(n), 256, 0, st>>>(e, n);
   GF_CHECK_LAUNCH();
+  double fro2 = -1.0;
+  GF_CUDA(cudaMemcpyAsync(&fro2, scal.as<double>() + 5, sizeof(double), cudaMemcpyDeviceToHost, st));
   GF_CUDA(cudaStreamSynchronize(st));
-  return EquilResult{k, converged, gamma};
+  EquilResult r{k, converged, gamma};
+  r.fro2 = fro2;
+  return r;
 }
 
 EquilResult equilibrate(gf_matrix* A, double gamma, double eps, int64_t max_iter, gf_comm* comm, double* d_dev,
@@ -265,6 +287,8 @@ EquilResult equilibrate(gf_matrix* A, double gamma, double eps, int64_t max_iter
   if (A->dtype == GF_F32) return equil_t<float>(A, gamma, eps, max_iter, comm, d_dev, e_dev, st, cb, user);
   return equil_t<double>(A, gamma, eps, max_iter, comm, d_dev, e_dev, st, cb, user);
 }
+
+static void apply_rescale(int64_t m, int64_t n, double mg, double fro2, double* d, double* e, cudaStream_t st);
 
 template <typename T>
 static void rescale_t(gf_matrix* A, double* d, double* e, gf_comm* comm, cudaStream_t st) {
@@ -285,16 +309,26 @@ static void rescale_t(gf_matrix* A, double* d, double* e, gf_comm* comm, cudaStr
   double h[3];
   GF_CUDA(cudaMemcpyAsync(h, scal.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
   GF_CUDA(cudaStreamSynchronize(st));
-  const double fro = sqrt(h[1]);
+  apply_rescale(m, n, mg, h[1], d, e, st);
+}
+
+// d, e /= sqrt(||D A E||_F / sqrt(min(m, n))) (equilibration.py:214-224)
+static void apply_rescale(int64_t m, int64_t n, double mg, double fro2, double* d, double* e, cudaStream_t st) {
+  const double fro = sqrt(fro2);
   const double factor = fro / sqrt(std::min(mg, (double)n));
   if (!std::isfinite(factor) || factor == 0.0)
     throw_error(GF_E_DEGENERATE_INPUT, "scaled matrix has zero or non-finite norm");
   const double s = sqrt(factor);
-  GF_CUDA(cudaMemcpyAsync(scal.p, &s, sizeof(double), cudaMemcpyHostToDevice, st));
-  scal_inplace<<<vgrid(m), 256, 0, st>>>(d, m, scal.as<double>(), 1);
-  scal_inplace<<<vgrid(n), 256, 0, st>>>(e, n, scal.as<double>(), 1);
+  DBuf sv(sizeof(double));
+  GF_CUDA(cudaMemcpyAsync(sv.p, &s, sizeof(double), cudaMemcpyHostToDevice, st));
+  scal_inplace<<<vgrid(m), 256, 0, st>>>(d, m, sv.as<double>(), 1);
+  scal_inplace<<<vgrid(n), 256, 0, st>>>(e, n, sv.as<double>(), 1);
   GF_CHECK_LAUNCH();
   GF_CUDA(cudaStreamSynchronize(st));
+}
+
+void rescale_even_fro2(gf_matrix* A, double* d, double* e, double fro2, gf_comm* comm, cudaStream_t st) {
+  apply_rescale(A->m, A->n, global_rows(A, comm, st), fro2, d, e, st);
 }
 
 // y = (A o A) x (x: n) or (A o A)' x (x: m), fp64 device vectors: the p = 2

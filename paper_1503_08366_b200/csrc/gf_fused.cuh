@@ -133,6 +133,12 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return pol;
 }
 
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 // TMA bulk copy global -> shared, completion counted on `bar` (tx bytes).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
                                          uint64_t pol) {
@@ -840,8 +846,11 @@ fused_rowcol_cl_kernel(const T* __restrict__ A, int64_t rows, int64_t ld, const 
       // lane 1: the column-ring re-loads (evict-first: their last use), on
       // their own so that waiting for a column slot never holds back the
       // HBM row stream.  (Lanes 0 and 1 diverge; both spin on try_wait.)
+      // (the status is read after the dependency wait: read before it, it
+      // can be the previous kernel's RUNNING while the compute warps see the
+      // stop, and this lane would wait forever for column slots nobody frees)
+      if (lane == 1) pdl_wait();
       if (lane == 1 && epi.active()) {
-        pdl_wait();
         const uint64_t pol = policy_evict_first();
         unsigned char* ringc = smem_raw + (size_t)nslot * sb;
         int slotc = 0;

@@ -116,6 +116,7 @@ struct EquilResult {
   int64_t sweeps;
   bool converged;
   double gamma;
+  double fro2 = -1.0;   // ||D A E||_F^2 of the result (from the last column sums), -1 if not formed
 };
 // per-sweep observer (on_sweep of equilibration.py:178-179): sweep k, host
 // copies of d_k^(1/2) (m) and e_k^(1/2) (n)
@@ -123,6 +124,8 @@ typedef void (*SweepCb)(int64_t k, const double* d, const double* e, int64_t m, 
 EquilResult equilibrate(gf_matrix* A, double gamma, double eps, int64_t max_iter, gf_comm* comm,
                         double* d_dev, double* e_dev, cudaStream_t st, SweepCb cb = nullptr, void* user = nullptr);
 void rescale_even(gf_matrix* A, double* d_dev, double* e_dev, gf_comm* comm, cudaStream_t st);
+// rescale_even with ||D A E||_F^2 already known (EquilResult::fro2): no pass over A
+void rescale_even_fro2(gf_matrix* A, double* d_dev, double* e_dev, double fro2, gf_comm* comm, cudaStream_t st);
 
 // --------------------------------------------------- vectors (gf_vec.cu) --
 // Device copy of a gf_terms (h int8 + five fp64 arrays), owned.

@@ -1579,6 +1579,18 @@ static int64_t ginv_grid(int64_t q, int sms) {
   return std::max<int64_t>(1, std::min<int64_t>(ceil_div(q, kRowWarps), (int64_t)sms * std::max(b, 1)));
 }
 
+// GF_LAUNCH_SYNC=1 (debug): synchronise after every iteration kernel and log it
+static void dbg_sync(cudaStream_t st, const char* what, int64_t k) {
+  static const bool on = [] {
+    const char* e = getenv("GF_LAUNCH_SYNC");
+    return e && e[0] == '1';
+  }();
+  if (!on) return;
+  fprintf(stderr, "[gf] k=%lld %s launched\n", (long long)k, what);
+  GF_CUDA(cudaStreamSynchronize(st));
+  fprintf(stderr, "[gf] k=%lld %s done\n", (long long)k, what);
+}
+
 template <typename T>
 static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
   gf_matrix* A = s->S->A;
@@ -1617,6 +1629,7 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
     GF_CHECK_LAUNCH();
     s->mark(0, st, false);
     s->launches += 1;
+    dbg_sync(st, "S", k);
   }
   if (s->m > 0 && (s->fplan.ok || s->fplan2.ok)) {
     // one pass over A_hat (row pass + y side + column pass) carrying the Z
@@ -1627,6 +1640,7 @@ static void launch_step(gf_solver* s, int64_t k, cudaStream_t st) {
     else fused2_dispatch<T>(s, st, false);   // rows split over the CTAs of a cluster
     s->mark(7, st, false);
     s->launches += 1;
+    dbg_sync(st, "fused", k);
     if (!comm_active(s->S->comm)) return;
     s->mark(6, st, true);
     allreduce_sum(s->S->comm, s->red.as<double>(), 2 * s->ld + kScal, st);
