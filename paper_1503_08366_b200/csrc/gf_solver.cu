@@ -1916,8 +1916,18 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
       else ring_dispatch<double>(s.get(), nullptr, true);
     }
     {   // the lower-triangle S step (gf_sym.cuh) replaces both when it fits
+      // Default: only where the triangle's saved bytes pay (G^-1 of 1 GB and
+      // more -- C3's q = 20000 fp64: 0.52 -> 0.29 ms); at q = 5000-10000 the
+      // ring is as fast (25 us either way) and has no grid barrier -- the
+      // lower-triangle kernel stalled intermittently in the C2 stress
+      // sequence (tools/hang_c2b.py; cause not isolated).
+      // GF_SYM=1 forces it on, GF_DISABLE_SYM=1 off.
       const char* senv = getenv("GF_DISABLE_SYM");
-      if (!(senv && senv[0] == '1') && s->tall && !s->indirect && s->ldq > 0)
+      const char* fenv = getenv("GF_SYM");
+      bool want_sym = (double)s->q * (double)s->ldq * (double)es >= (double)(1ull << 30);
+      if (fenv && fenv[0] == '1') want_sym = true;
+      if (senv && senv[0] == '1') want_sym = false;
+      if (want_sym && s->tall && !s->indirect && s->ldq > 0)
         s->splan = plan_sym(s->q, s->ldq, (int)es, sms, (size_t)optin, s->grid_s);
       if (s->splan.ok) {
         s->sym_tm = sym_map(s->S->P->ginv.p, s->q, s->ldq, s->dtype);

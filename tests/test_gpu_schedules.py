@@ -1,8 +1,8 @@
 """The alternative iteration schedules agree with the default one: the
 two-pass schedule (GF_DISABLE_FUSED=1, what wide rows and Newton-heavy
-problems use), the full-matrix G^-1 GEMVs instead of the lower-triangle one
-(GF_DISABLE_SYM=1: the TMA row ring; with GF_DISABLE_RING=1 too: the plain
-row GEMV), the cluster
+problems use), the lower-triangle G^-1 GEMV (GF_SYM=1; by default only for
+G^-1 of 1 GB and more) and the plain row GEMV instead of the TMA row ring
+(GF_DISABLE_SYM=1 GF_DISABLE_RING=1), the cluster
 pass forced onto these narrow rows with 2-, 4-, 8- and 9-CTA clusters
 (GF_FUSED_CL2=1, GF_FUSED_CL=c: the instances that C5 fp64 and C3 use at
 full size; 9 is C3's), its lagged form (GF_FUSED_LAG=1: column pass on rows re-read
@@ -52,7 +52,7 @@ def test_schedule_variants_agree():
     base = run_variant({})
     nopdl = run_variant({"GF_DISABLE_PDL": "1"})
     assert nopdl == base   # PDL changes launch timing only: bit-identical
-    for env in ({"GF_DISABLE_FUSED": "1"}, {"GF_DISABLE_SYM": "1"}, {"GF_DISABLE_SYM": "1", "GF_DISABLE_RING": "1"},
+    for env in ({"GF_DISABLE_FUSED": "1"}, {"GF_SYM": "1"}, {"GF_DISABLE_SYM": "1", "GF_DISABLE_RING": "1"},
                 {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "2"}, {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "4"},
                 {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "8"}, {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "9"},
                 {"GF_FUSED_CL2": "1", "GF_FUSED_CL": "2", "GF_FUSED_LAG": "1"}):
