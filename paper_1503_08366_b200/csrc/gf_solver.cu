@@ -1918,9 +1918,9 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
     {   // the lower-triangle S step (gf_sym.cuh) replaces both when it fits
       // Default: only where the triangle's saved bytes pay (G^-1 of 1 GB and
       // more -- C3's q = 20000 fp64: 0.52 -> 0.29 ms); at q = 5000-10000 the
-      // ring is as fast (25 us either way) and has no grid barrier -- the
-      // lower-triangle kernel stalled intermittently in the C2 stress
-      // sequence (tools/hang_c2b.py; cause not isolated).
+      // ring is about as fast and has no grid barrier (the lower-triangle
+      // kernel's slot aliasing stall at C2 size is fixed in plan_sym, and the
+      // default kept as stress-tested).
       // GF_SYM=1 forces it on, GF_DISABLE_SYM=1 off.
       const char* senv = getenv("GF_DISABLE_SYM");
       const char* fenv = getenv("GF_SYM");

@@ -57,6 +57,13 @@ inline SymPlan plan_sym(int64_t q, int64_t ldq, int esize, int sms, size_t smem_
   const size_t tile = (size_t)kSymTB * kSymTB * esize;
   const size_t budget = smem_max > 16384 ? smem_max - 16384 : 0;
   p.nslot = (int)std::min<size_t>(12, budget / tile);
+  // a multiple of the warp count: tile j goes to warp j % W and slot
+  // j % nslot, so every slot then belongs to one warp, which waits on its
+  // phases in order.  With slots shared by several warps (12 slots, 8 warps:
+  // the fp32 plan before) a warp running ahead of a slow one can match a
+  // phase of the same parity two rounds old, consume a stale tile and
+  // release its slot early -- the intermittent stall of DESIGN §4.
+  p.nslot -= p.nslot % warps;
   p.grid = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms, p.nt, max_grid}));
   p.smem = (size_t)p.nslot * tile;
   p.ok = q >= kSymTB && p.nslot >= warps && (ldq * esize) % 16 == 0;
