@@ -1916,15 +1916,14 @@ gf_solver* solver_create(gf_setup* S, const gf_terms* f, const gf_terms* g, cons
       else ring_dispatch<double>(s.get(), nullptr, true);
     }
     {   // the lower-triangle S step (gf_sym.cuh) replaces both when it fits
-      // Default: only where the triangle's saved bytes pay (G^-1 of 1 GB and
-      // more -- C3's q = 20000 fp64: 0.52 -> 0.29 ms); at q = 5000-10000 the
-      // ring is about as fast and has no grid barrier (the lower-triangle
-      // kernel's slot aliasing stall at C2 size is fixed in plan_sym, and the
-      // default kept as stress-tested).
+      // Default: where the triangle's saved bytes pay -- G^-1 of 256 MB and
+      // more (C3's q = 20000 fp64: 0.52 -> 0.29 ms; C2's q = 10000 fp32:
+      // 67 -> 61 us); at q = 5000 (100 MB) the ring is as fast (24.7 vs
+      // 25.9 us) and has no grid barrier.
       // GF_SYM=1 forces it on, GF_DISABLE_SYM=1 off.
       const char* senv = getenv("GF_DISABLE_SYM");
       const char* fenv = getenv("GF_SYM");
-      bool want_sym = (double)s->q * (double)s->ldq * (double)es >= (double)(1ull << 30);
+      bool want_sym = (double)s->q * (double)s->ldq * (double)es >= (double)(256ull << 20);
       if (fenv && fenv[0] == '1') want_sym = true;
       if (senv && senv[0] == '1') want_sym = false;
       if (want_sym && s->tall && !s->indirect && s->ldq > 0)

@@ -1,7 +1,7 @@
 """The alternative iteration schedules agree with the default one: the
 two-pass schedule (GF_DISABLE_FUSED=1, what wide rows and Newton-heavy
 problems use), the lower-triangle G^-1 GEMV (GF_SYM=1; by default only for
-G^-1 of 1 GB and more) and the plain row GEMV instead of the TMA row ring
+G^-1 of 256 MB and more) and the plain row GEMV instead of the TMA row ring
 (GF_DISABLE_SYM=1 GF_DISABLE_RING=1), the cluster
 pass forced onto these narrow rows with 2-, 4-, 8- and 9-CTA clusters
 (GF_FUSED_CL2=1, GF_FUSED_CL=c: the instances that C5 fp64 and C3 use at

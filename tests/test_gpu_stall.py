@@ -49,7 +49,7 @@ print("done", flush=True)
 
 @pytest.mark.parametrize("pdl", ["on", "off"])
 def test_no_stall_lagged_pass_and_s_step(pdl):
-    """Default schedules (the S step on the TMA row ring at this q)."""
+    """Default schedules (the lower-triangle S step at this q)."""
     env = dict(os.environ)
     if pdl == "off":
         env["GF_DISABLE_PDL"] = "1"
